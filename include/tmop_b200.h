@@ -1,0 +1,173 @@
+/*
+ * tmop_b200.h -- C ABI of the B200-native TMOP hot path (libtmop_b200.so).
+ *
+ * This is the drop-in boundary for the reference package's `ProblemLike`
+ * operator protocol (/root/reference/pkg/src/tmopbench/solvers.py:183-189)
+ * and its concrete implementer `TmopProblem`
+ * (/root/reference/pkg/src/tmopbench/operator.py:220-459).  Every entry point
+ * takes plain device pointers and sizes, is asynchronous on the context's
+ * CUDA stream and returns an int status (TMOP_OK == 0).  No torch types.
+ *
+ * Vector conventions follow the reference (operator.py:10-13, fe.py:1-14):
+ * T-vectors are (dim * n_nodes) float64, component-major; node ids and
+ * element ids are lexicographic with x fastest; restriction is int32
+ * (n_elements, (order+1)^dim) with the local x index fastest.
+ *
+ * Q-data (the partially assembled Hessian, reference HessQData
+ * operator.py:91-138) is stored ELEMENT-BLOCKED: qdata[e][field][q],
+ * fields = tmop_qdata_fields(ctx) doubles per quadrature point.  For the
+ * template metrics (mu_2, mu_7, mu_55, mu_303) the fields are
+ * c_id, c_ts, c_ss, c_x (scaled by w_q * coef), S (d*d), T (d*d) -- the
+ * reference's 4 + 2 d^2 values per point, in the reference order.  For
+ * mu_302 / mu_321 (no reference equivalent) the fields are w (1), S, T.
+ */
+#ifndef TMOP_B200_H
+#define TMOP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  TMOP_OK = 0,
+  TMOP_ERR_ARG = 1,          /* invalid argument / unsupported (dim, p, n_q) */
+  TMOP_ERR_CUDA = 2,         /* a CUDA runtime call failed */
+  TMOP_ERR_METRIC = 3,       /* metric id not valid for this dimension */
+};
+
+/* Metric ids: 2, 55, 303 follow metrics.py:41-44; 7, 302, 321 are the
+ * MFEM-numbered extensions named by BASELINE.json (no reference code). */
+enum { TMOP_MU_2 = 2, TMOP_MU_7 = 7, TMOP_MU_55 = 55, TMOP_MU_302 = 302,
+       TMOP_MU_303 = 303, TMOP_MU_321 = 321 };
+
+typedef struct tmop_ctx tmop_ctx;
+
+/* Determinant status written by kernels that evaluate det(A) (device
+ * memory).  min_det = min over all quadrature points of det(A); argmin is
+ * the flat point index e * Q + q of the first minimum (ties -> smallest). */
+typedef struct {
+  double min_det;
+  int64_t argmin;
+} tmop_det_status;
+
+/* ---- context (replaces TmopProblem.__init__, operator.py:230-250) ------ */
+
+/* Create a context.  restriction/fixed/l2e_* are DEVICE pointers owned by
+ * the caller and must outlive the context.  B, G are HOST (n_quad x
+ * (order+1)) row-major tables B[q][i] = l_i(chi_q), G[q][i] = l_i'(chi_q)
+ * (fe.py:143-160); w1 is the HOST 1D quadrature weight vector (n_quad)
+ * (fe.py:126-140).  fixed is uint8 per node, bit a set <=> component a
+ * constrained (mesh.py:159-160).  l2e_offsets (n_nodes + 1, int64) and
+ * l2e_index (n_elements * (order+1)^dim, uint32 = e * Np + local) give, for
+ * every node, its element-local copies in ascending element order -- the
+ * summation order of np.add.at in fe.py:189-204.  stream is a
+ * cudaStream_t (NULL = legacy default stream). */
+int tmop_ctx_create(tmop_ctx **out, int dim, int order, int n_quad,
+                    int64_t n_elements, int64_t n_nodes,
+                    const int32_t *restriction, const uint8_t *fixed,
+                    const int64_t *l2e_offsets, const uint32_t *l2e_index,
+                    const double *B, const double *G, const double *w1,
+                    int metric, double inv_scale, double det_w,
+                    double spatial_weight, void *stream);
+int tmop_ctx_destroy(tmop_ctx *ctx);
+int tmop_ctx_set_stream(tmop_ctx *ctx, void *stream);
+/* Change target scale (build_targets, metrics.py:333-345) after creation. */
+int tmop_ctx_set_target(tmop_ctx *ctx, double inv_scale, double det_w);
+int tmop_qdata_fields(const tmop_ctx *ctx);            /* doubles per point */
+int64_t tmop_qdata_size(const tmop_ctx *ctx);          /* doubles total     */
+/* Configure the displacement-limiting term (operator.py:57-76, 463-533):
+ * x0 (reference positions, T-vector) and delta_nodal (n_nodes, or NULL for
+ * the scalar delta) are DEVICE pointers; weight > 0 enables, 0 disables. */
+int tmop_ctx_set_limiting(tmop_ctx *ctx, const double *x0,
+                          const double *delta_nodal, double delta,
+                          double weight);
+const char *tmop_last_error(void);
+
+/* ---- operator entry points (all async on the context stream) ---------- */
+
+/* AssembleGradPA: hessian_setup (operator.py:350-371). */
+int tmop_hessian_setup(tmop_ctx *ctx, const double *x, double *qdata,
+                       tmop_det_status *det_out);
+/* AddMultGradPA: hessian_apply (operator.py:401-418).  y = H vin on free
+ * dofs, y = v on constrained dofs. */
+int tmop_hessian_apply(tmop_ctx *ctx, const double *qdata, const double *v,
+                       double *y);
+/* AssembleGradDiagonalPA: hessian_diagonal (operator.py:420-459). */
+int tmop_hessian_diagonal(tmop_ctx *ctx, const double *qdata, double *diag);
+/* AddMultPA: gradient (operator.py:328-346). */
+int tmop_gradient(tmop_ctx *ctx, const double *x, double *grad,
+                  tmop_det_status *det_out);
+/* GetLocalStateEnergyPA: objective (operator.py:311-326).  Writes F (incl.
+ * the limiting term when configured) to *energy_out (device). */
+int tmop_objective(tmop_ctx *ctx, const double *x, double *energy_out,
+                   tmop_det_status *det_out);
+/* min_det_jacobian (operator.py:296-304). */
+int tmop_min_det(tmop_ctx *ctx, const double *x, tmop_det_status *det_out);
+/* Per-element min det(A) and its point (diagnostics / exact batch
+ * emulation of operator.py:267-272).  elem_min: n_elements doubles,
+ * elem_arg: n_elements int32 (device). */
+int tmop_element_min_det(tmop_ctx *ctx, const double *x, double *elem_min,
+                         int32_t *elem_arg);
+/* Volume of the mesh image by quadrature of det(A) (metrics.py:319-330). */
+int tmop_volume(tmop_ctx *ctx, const double *x, double *vol_out);
+
+/* Pointwise metric evaluation for n matrices T (n, d, d) row-major:
+ * mu (n), P = dmu/dT (n, d, d), H = d2mu/dT2 (n, d*d, d*d); any output may
+ * be NULL.  Device pointers, default stream, synchronous. */
+int tmop_metric_eval(int metric, int dim, int64_t n, const double *T,
+                     double *mu, double *P, double *H);
+
+/* ---- vector kernels for the device MINRES / Newton (solvers.py) ------- */
+
+/* Deterministic dot product (fixed-order two-pass reduction) -> *out (dev). */
+int tmop_dot(tmop_ctx *ctx, int64_t n, const double *a, const double *b,
+             double *out);
+/* y = a * x + b * y (AXPBY). */
+int tmop_axpby(tmop_ctx *ctx, int64_t n, double a, const double *x, double b,
+               double *y);
+/* out = x - alpha * dx (line search trial point, solvers.py:210). */
+int tmop_trial_point(tmop_ctx *ctx, int64_t n, const double *x,
+                     const double *dx, double alpha, double *out);
+/* inv = 1 / max(|diag|, floor) (solvers.py:83-90); *nonfinite (dev int)
+ * is set to 1 if any diag entry is not finite. */
+int tmop_jacobi_inverse(tmop_ctx *ctx, int64_t n, const double *diag,
+                        double floor_value, double *inv, int32_t *nonfinite);
+
+/* Device-resident MINRES state (solvers.py:93-180).  All scalars live in
+ * device memory so an iteration needs no host round trip; `done` makes every
+ * later step a no-op, so the host may launch several steps per check. */
+typedef struct {
+  double beta1, beta, oldb, alfa, beta2, dbar, epsln, sn, cs, phibar,
+         relres, gamma;
+  int32_t itn, done, breakdown, nonpd;
+} tmop_minres_state;
+
+/* Initialise (slot 0 of st2): r1 = r2 = b; z = inv .* b (z = b if inv == NULL);
+ * beta1 = sqrt(b.z); v = z / beta1; x = w = w2 = 0; st set up as in
+ * solvers.py:103-125 (done = 1 when beta1 == 0). */
+int tmop_minres_init(tmop_ctx *ctx, int64_t n, const double *b,
+                     const double *inv, double *x, double *r1, double *r2,
+                     double *z, double *v, double *w, double *w2,
+                     tmop_minres_state *st2);
+/* One MINRES iteration after the caller computed Av = A v (solvers.py:
+ * 131-178).  Fused kernels: Av -= (beta/oldb) r1; alfa = v.Av;
+ * Av -= (alfa/beta) r2; z = inv .* Av; beta2 = Av.z; Givens recurrence;
+ * w1buf <- (v - oldeps w2 - delta w) / gamma; x += phi w1buf;
+ * v <- z / beta.  The caller then rotates buffers:
+ *   (r1, r2, free) <- (r2, Av, r1) and (w1, w2, w) <- (w2, w, w1buf).
+ * st2 points to TWO state slots (device); init writes slot 0 and step k
+ * (0-based) reads slot k&1 and writes slot (k+1)&1, so after K steps the
+ * current state is slot K&1. */
+int tmop_minres_step(tmop_ctx *ctx, int64_t n, double *Av, const double *r1,
+                     const double *r2, const double *inv, double *z,
+                     double *v, const double *w, double *w1buf,
+                     const double *w2, double *x, double rtol,
+                     tmop_minres_state *st2, int k);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TMOP_B200_H */

@@ -1,0 +1,364 @@
+// tmop_capi.cu -- the extern "C" boundary (include/tmop_b200.h).
+//
+// The context replaces TmopProblem.__init__ (operator.py:230-250): it holds
+// the discretisation constants (1D tables as a by-value kernel parameter),
+// the caller-owned device mesh arrays, and library-owned scratch (the
+// element-blocked E-vector and the per-CTA reduction partials).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/tmop_b200.h"
+#include "tmop_core.h"
+#include "tmop_elem.cuh"
+#include "tmop_internal.h"
+
+using namespace tmop;
+
+static thread_local char g_err[512] = "";
+
+static int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) return fail(TMOP_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+struct tmop_ctx {
+  int dim, order, n1, nq, QP, NP;
+  int64_t ne, nn;
+  const int32_t *restr;
+  const uint8_t *fixed;
+  const int64_t *l2e_off;
+  const uint32_t *l2e_idx;
+  Tab tab;
+  int metric;
+  double omega, det_w, inv_s;
+  cudaStream_t stream;
+  double *E;
+  double *part_sum, *part_min;
+  int64_t *part_arg;
+  double *vpart1, *vpart2;
+};
+
+namespace tmop {
+int launch_elem(int dim, int n1, int nq, int kind, ElemArgs &a, const Tab &t, cudaStream_t s) {
+  if (dim == 2) return launch_elem_2d(n1, nq, kind, a, t, s);
+  switch (n1) {
+    case 2: return launch_elem_3d_n2(nq, kind, a, t, s);
+    case 3: return launch_elem_3d_n3(nq, kind, a, t, s);
+    case 4: return launch_elem_3d_n4(nq, kind, a, t, s);
+    case 5: return launch_elem_3d_n5(nq, kind, a, t, s);
+    default: return -1;
+  }
+}
+bool elem_supported(int dim, int n1, int nq) {
+  return (dim == 2 || dim == 3) && n1 >= 2 && n1 <= MAXN && nq >= 2 && nq <= MAXQ;
+}
+}  // namespace tmop
+
+static bool metric_ok(int metric, int dim) {
+  switch (metric) {
+    case MU2:
+    case MU7: return dim == 2;
+    case MU55: return true;
+    case MU302:
+    case MU303:
+    case MU321: return dim == 3;
+    default: return false;
+  }
+}
+
+static ElemArgs base_args(const tmop_ctx *c) {
+  ElemArgs a;
+  memset(&a, 0, sizeof(a));
+  a.ne = c->ne;
+  a.nn = c->nn;
+  a.restr = c->restr;
+  a.fixed = c->fixed;
+  a.metric = c->metric;
+  const double is = c->inv_s;
+  a.inv_s = is;
+  a.inv_s_dm1 = c->dim == 3 ? is * is : is;
+  a.inv_s_d = c->dim == 3 ? is * is * is : is * is;
+  a.coef_e = c->omega * c->det_w;
+  a.coef_g = c->omega * c->det_w * is;
+  a.coef_h = c->omega * c->det_w * (is * is);
+  a.E = c->E;
+  a.part_sum = c->part_sum;
+  a.part_min = c->part_min;
+  a.part_arg = c->part_arg;
+  return a;
+}
+
+static int run(tmop_ctx *c, int kind, ElemArgs &a, int *grid_out) {
+  const int g = launch_elem(c->dim, c->n1, c->nq, kind, a, c->tab, c->stream);
+  if (g < 0) return fail(TMOP_ERR_ARG, "no kernel instance for dim=%d p=%d n_q=%d (kind %d)", c->dim, c->order, c->nq, kind);
+  CUDA_TRY(cudaGetLastError());
+  if (grid_out) *grid_out = g;
+  return TMOP_OK;
+}
+
+extern "C" {
+
+const char *tmop_last_error(void) { return g_err; }
+
+int tmop_ctx_create(tmop_ctx **out, int dim, int order, int n_quad, int64_t n_elements, int64_t n_nodes,
+                    const int32_t *restriction, const uint8_t *fixed, const int64_t *l2e_offsets,
+                    const uint32_t *l2e_index, const double *B, const double *G, const double *w1, int metric,
+                    double inv_scale, double det_w, double spatial_weight, void *stream) {
+  if (!out) return fail(TMOP_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (!elem_supported(dim, order + 1, n_quad))
+    return fail(TMOP_ERR_ARG, "unsupported (dim=%d, p=%d, n_q=%d): need dim in {2,3}, 1<=p<=%d, 2<=n_q<=%d", dim,
+                order, n_quad, MAXN - 1, MAXQ);
+  if (!metric_ok(metric, dim)) return fail(TMOP_ERR_METRIC, "metric %d is not valid in %dD", metric, dim);
+  if (n_elements < 0 || n_nodes < 0) return fail(TMOP_ERR_ARG, "negative sizes");
+  const int np = (int)std::lround(std::pow(order + 1, dim));
+  if ((double)n_elements * np >= 4294967295.0) return fail(TMOP_ERR_ARG, "mesh too large for uint32 E-indices");
+  tmop_ctx *c = new (std::nothrow) tmop_ctx;
+  if (!c) return fail(TMOP_ERR_ARG, "out of host memory");
+  memset(c, 0, sizeof(*c));
+  c->dim = dim;
+  c->order = order;
+  c->n1 = order + 1;
+  c->nq = n_quad;
+  c->NP = np;
+  c->QP = (int)std::lround(std::pow(n_quad, dim));
+  c->ne = n_elements;
+  c->nn = n_nodes;
+  c->restr = restriction;
+  c->fixed = fixed;
+  c->l2e_off = l2e_offsets;
+  c->l2e_idx = l2e_index;
+  for (int q = 0; q < n_quad; ++q) {
+    for (int i = 0; i < c->n1; ++i) {
+      c->tab.B[q * c->n1 + i] = B[q * c->n1 + i];
+      c->tab.G[q * c->n1 + i] = G[q * c->n1 + i];
+    }
+    c->tab.w1[q] = w1[q];
+  }
+  c->metric = metric;
+  c->omega = spatial_weight;
+  c->det_w = det_w;
+  c->inv_s = inv_scale;
+  c->stream = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  const size_t esz = (size_t)n_elements * dim * np;
+  e = cudaMalloc(&c->E, (esz ? esz : 1) * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c->part_sum, GRID_CAP * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c->part_min, GRID_CAP * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c->part_arg, GRID_CAP * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->vpart1, VEC_GRID_CAP * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c->vpart2, VEC_GRID_CAP * sizeof(double));
+  if (e != cudaSuccess) {
+    tmop_ctx_destroy(c);
+    return fail(TMOP_ERR_CUDA, "workspace allocation failed: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return TMOP_OK;
+}
+
+int tmop_ctx_destroy(tmop_ctx *c) {
+  if (!c) return TMOP_OK;
+  cudaFree(c->E);
+  cudaFree(c->part_sum);
+  cudaFree(c->part_min);
+  cudaFree(c->part_arg);
+  cudaFree(c->vpart1);
+  cudaFree(c->vpart2);
+  delete c;
+  return TMOP_OK;
+}
+
+int tmop_ctx_set_stream(tmop_ctx *c, void *stream) {
+  if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
+  c->stream = (cudaStream_t)stream;
+  return TMOP_OK;
+}
+
+int tmop_ctx_set_target(tmop_ctx *c, double inv_scale, double det_w) {
+  if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
+  if (!(inv_scale > 0.0) || !(det_w > 0.0)) return fail(TMOP_ERR_ARG, "target scale must be positive");
+  c->inv_s = inv_scale;
+  c->det_w = det_w;
+  return TMOP_OK;
+}
+
+int tmop_qdata_fields(const tmop_ctx *c) {
+  if (!c) return -1;
+  return metric_is_template(c->metric) ? 4 + 2 * c->dim * c->dim : 1 + 2 * c->dim * c->dim;
+}
+
+int64_t tmop_qdata_size(const tmop_ctx *c) {
+  if (!c) return -1;
+  return (int64_t)tmop_qdata_fields(c) * c->QP * c->ne;
+}
+
+int tmop_ctx_set_limiting(tmop_ctx *c, const double *, const double *, double, double) {
+  if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
+  return fail(TMOP_ERR_ARG, "limiting term not available in this build");
+}
+
+int tmop_hessian_setup(tmop_ctx *c, const double *x, double *qdata, tmop_det_status *det_out) {
+  if (!c || !x || !qdata || !det_out) return fail(TMOP_ERR_ARG, "NULL argument");
+  ElemArgs a = base_args(c);
+  a.in = x;
+  a.qout = qdata;
+  int g = 0;
+  int rc = run(c, K_SETUP, a, &g);
+  if (rc) return rc;
+  launch_fin(g, nullptr, c->part_min, c->part_arg, 0.0, nullptr, 0.0, nullptr, det_out, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_hessian_apply(tmop_ctx *c, const double *qdata, const double *v, double *y) {
+  if (!c || !qdata || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
+  ElemArgs a = base_args(c);
+  a.in = v;
+  a.qdata = qdata;
+  int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
+  if (rc) return rc;
+  launch_e2l(c->dim, c->nn, c->NP, c->l2e_off, c->l2e_idx, c->E, c->fixed, 0, v, nullptr, y, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_hessian_diagonal(tmop_ctx *c, const double *qdata, double *diag) {
+  if (!c || !qdata || !diag) return fail(TMOP_ERR_ARG, "NULL argument");
+  ElemArgs a = base_args(c);
+  a.qdata = qdata;
+  int rc = run(c, metric_is_template(c->metric) ? K_DIAG : K_DIAG_NT, a, nullptr);
+  if (rc) return rc;
+  launch_e2l(c->dim, c->nn, c->NP, c->l2e_off, c->l2e_idx, c->E, c->fixed, 2, nullptr, nullptr, diag, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_gradient(tmop_ctx *c, const double *x, double *grad, tmop_det_status *det_out) {
+  if (!c || !x || !grad || !det_out) return fail(TMOP_ERR_ARG, "NULL argument");
+  ElemArgs a = base_args(c);
+  a.in = x;
+  int g = 0;
+  int rc = run(c, K_GRAD, a, &g);
+  if (rc) return rc;
+  launch_e2l(c->dim, c->nn, c->NP, c->l2e_off, c->l2e_idx, c->E, c->fixed, 1, nullptr, nullptr, grad, c->stream);
+  launch_fin(g, nullptr, c->part_min, c->part_arg, 0.0, nullptr, 0.0, nullptr, det_out, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_objective(tmop_ctx *c, const double *x, double *energy_out, tmop_det_status *det_out) {
+  if (!c || !x || !energy_out || !det_out) return fail(TMOP_ERR_ARG, "NULL argument");
+  ElemArgs a = base_args(c);
+  a.in = x;
+  int g = 0;
+  int rc = run(c, K_ENERGY, a, &g);
+  if (rc) return rc;
+  launch_fin(g, c->part_sum, c->part_min, c->part_arg, a.coef_e, energy_out, 0.0, nullptr, det_out, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_min_det(tmop_ctx *c, const double *x, tmop_det_status *det_out) {
+  if (!c || !x || !det_out) return fail(TMOP_ERR_ARG, "NULL argument");
+  ElemArgs a = base_args(c);
+  a.in = x;
+  int g = 0;
+  int rc = run(c, K_MINDET, a, &g);
+  if (rc) return rc;
+  launch_fin(g, nullptr, c->part_min, c->part_arg, 0.0, nullptr, 0.0, nullptr, det_out, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_element_min_det(tmop_ctx *c, const double *x, double *elem_min, int32_t *elem_arg) {
+  if (!c || !x || !elem_min || !elem_arg) return fail(TMOP_ERR_ARG, "NULL argument");
+  ElemArgs a = base_args(c);
+  a.in = x;
+  a.elem_min = elem_min;
+  a.elem_arg = elem_arg;
+  return run(c, K_ELEMDET, a, nullptr);
+}
+
+int tmop_volume(tmop_ctx *c, const double *x, double *vol_out) {
+  if (!c || !x || !vol_out) return fail(TMOP_ERR_ARG, "NULL argument");
+  ElemArgs a = base_args(c);
+  a.in = x;
+  int g = 0;
+  int rc = run(c, K_VOLUME, a, &g);
+  if (rc) return rc;
+  launch_fin(g, c->part_sum, nullptr, nullptr, 1.0, vol_out, 0.0, nullptr, nullptr, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_metric_eval(int metric, int dim, int64_t n, const double *T, double *mu, double *P, double *H) {
+  if (dim != 2 && dim != 3) return fail(TMOP_ERR_ARG, "dim must be 2 or 3");
+  if (!metric_ok(metric, dim)) return fail(TMOP_ERR_METRIC, "metric %d is not valid in %dD", metric, dim);
+  launch_metric_eval(metric, dim, n, T, mu, P, H);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaDeviceSynchronize());
+  return TMOP_OK;
+}
+
+int tmop_dot(tmop_ctx *c, int64_t n, const double *a, const double *b, double *out) {
+  if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
+  launch_dot(n, a, b, c->vpart1, out, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_axpby(tmop_ctx *c, int64_t n, double a, const double *x, double b, double *y) {
+  if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
+  launch_axpby(n, a, x, b, y, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_trial_point(tmop_ctx *c, int64_t n, const double *x, const double *dx, double alpha, double *out) {
+  if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
+  launch_trial(n, x, dx, alpha, out, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_jacobi_inverse(tmop_ctx *c, int64_t n, const double *diag, double floor_value, double *inv,
+                        int32_t *nonfinite) {
+  if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
+  launch_jacobi(n, diag, floor_value, inv, nonfinite, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_minres_init(tmop_ctx *c, int64_t n, const double *b, const double *inv, double *x, double *r1, double *r2,
+                     double *z, double *v, double *w, double *w2, tmop_minres_state *st2) {
+  if (!c || !st2) return fail(TMOP_ERR_ARG, "NULL argument");
+  launch_minres_init(n, b, inv, x, r1, r2, z, v, w, w2, c->vpart1, st2, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_minres_step(tmop_ctx *c, int64_t n, double *Av, const double *r1, const double *r2, const double *inv,
+                     double *z, double *v, const double *w, double *w1buf, const double *w2, double *x, double rtol,
+                     tmop_minres_state *st2, int k) {
+  if (!c || !st2) return fail(TMOP_ERR_ARG, "NULL argument");
+  launch_minres_step(n, Av, r1, r2, inv, z, v, w, w1buf, w2, x, rtol, st2 + (k & 1), st2 + ((k + 1) & 1), c->vpart1,
+                     c->vpart2, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,32 @@
+// tmop_core.h -- launchers implemented in tmop_core.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/tmop_b200.h"
+
+namespace tmop {
+
+constexpr int VEC_NT = 256;
+constexpr int VEC_GRID_CAP = 148 * 4;
+
+int vec_grid(int64_t n);
+int launch_e2l(int dim, int64_t nn, int np, const int64_t *off, const uint32_t *idx, const double *E,
+               const uint8_t *fixed, int mode, const double *v, const double *add, double *y, cudaStream_t s);
+void launch_fin(int nparts, const double *psum, const double *pmin, const int64_t *parg, double sum_scale,
+                double *sum_out, double add_scale, const double *add, tmop_det_status *det_out, cudaStream_t s);
+int launch_metric_eval(int metric, int dim, int64_t n, const double *T, double *mu, double *P, double *H);
+void launch_dot(int64_t n, const double *a, const double *b, double *part, double *out, cudaStream_t s);
+void launch_axpby(int64_t n, double a, const double *x, double b, double *y, cudaStream_t s);
+void launch_trial(int64_t n, const double *x, const double *dx, double alpha, double *out, cudaStream_t s);
+void launch_jacobi(int64_t n, const double *d, double fl, double *inv, int32_t *nonfinite, cudaStream_t s);
+void launch_minres_init(int64_t n, const double *b, const double *inv, double *x, double *r1, double *r2, double *z,
+                        double *v, double *w, double *w2, double *part, tmop_minres_state *st, cudaStream_t s);
+void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r2, const double *inv, double *z,
+                        double *v, const double *w, double *w1buf, const double *w2, double *x, double rtol,
+                        tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, double *part2,
+                        cudaStream_t s);
+
+}  // namespace tmop

@@ -1,0 +1,324 @@
+// tmop_device.cuh -- device building blocks of the B200 TMOP kernels.
+//
+// * Tab: 1D basis tables B[q][i], G[q][i] and 1D weights, passed BY VALUE
+//   as a __grid_constant__ kernel parameter so every table read is a
+//   constant-bank operand (no shared-memory or register pressure).
+//   (fe.py:143-160, fe.py:126-140)
+// * Point algebra: det / cofactor / metric values, first derivatives and the
+//   4-coefficient Hessian template (metrics.py:7-13, 173-262;
+//   _kernels.py:20-258), plus the non-template mu_302 / mu_321 Hessian
+//   actions (extensions, derived in DESIGN.md section 3).
+// * Sum-factorised stages over shared memory (fe.py:218-253 restated as
+//   per-line register-blocked contractions, one work item = one 1D line).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tmop {
+
+constexpr int MAXN = 5;   // p <= 4
+constexpr int MAXQ = 9;   // n_q <= 9 (paper table uses 9)
+
+struct Tab {
+  double B[MAXQ * MAXN];
+  double G[MAXQ * MAXN];
+  double w1[MAXQ];
+};
+
+template <int Q, int N>
+__device__ __forceinline__ double tB(const Tab &t, int q, int i) { return t.B[q * N + i]; }
+template <int Q, int N>
+__device__ __forceinline__ double tG(const Tab &t, int q, int i) { return t.G[q * N + i]; }
+
+// tensor weight of flat point q (x fastest): w[qz] * (w[qy] * w[qx]),
+// the association order of np.multiply.outer in fe.py:134-140.
+template <int DIM, int Q>
+__device__ __forceinline__ double wq(const Tab &t, int q) {
+  if constexpr (DIM == 2) {
+    return t.w1[q / Q] * t.w1[q % Q];
+  } else {
+    return t.w1[q / (Q * Q)] * (t.w1[(q / Q) % Q] * t.w1[q % Q]);
+  }
+}
+
+// ---------------------------------------------------------------- metrics
+enum : int { MU2 = 2, MU7 = 7, MU55 = 55, MU302 = 302, MU303 = 303, MU321 = 321 };
+
+__host__ __device__ inline bool metric_is_template(int m) {
+  return m == MU2 || m == MU7 || m == MU55 || m == MU303;
+}
+
+template <int D>
+__device__ __forceinline__ double mdet(const double (&A)[D][D]) {
+  if constexpr (D == 2) {
+    return A[0][0] * A[1][1] - A[0][1] * A[1][0];
+  } else {
+    return A[0][0] * (A[1][1] * A[2][2] - A[1][2] * A[2][1]) -
+           A[0][1] * (A[1][0] * A[2][2] - A[1][2] * A[2][0]) +
+           A[0][2] * (A[1][0] * A[2][1] - A[1][1] * A[2][0]);
+  }
+}
+
+// cof(A) with A^{-T} = cof(A)/det(A) (metrics.py:79-97, _kernels.py:115-131)
+template <int D>
+__device__ __forceinline__ void mcof(const double (&A)[D][D], double (&C)[D][D]) {
+  if constexpr (D == 2) {
+    C[0][0] = A[1][1];  C[0][1] = -A[1][0];
+    C[1][0] = -A[0][1]; C[1][1] = A[0][0];
+  } else {
+    C[0][0] = A[1][1] * A[2][2] - A[1][2] * A[2][1];
+    C[0][1] = A[1][2] * A[2][0] - A[1][0] * A[2][2];
+    C[0][2] = A[1][0] * A[2][1] - A[1][1] * A[2][0];
+    C[1][0] = A[0][2] * A[2][1] - A[0][1] * A[2][2];
+    C[1][1] = A[0][0] * A[2][2] - A[0][2] * A[2][0];
+    C[1][2] = A[0][1] * A[2][0] - A[0][0] * A[2][1];
+    C[2][0] = A[0][1] * A[1][2] - A[0][2] * A[1][1];
+    C[2][1] = A[0][2] * A[1][0] - A[0][0] * A[1][2];
+    C[2][2] = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+  }
+}
+
+template <int D>
+__device__ __forceinline__ double mfro2(const double (&A)[D][D]) {
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) s += A[i][j] * A[i][j];
+  return s;
+}
+
+template <int D>
+__device__ __forceinline__ double mdot(const double (&A)[D][D], const double (&B)[D][D]) {
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) s += A[i][j] * B[i][j];
+  return s;
+}
+
+// C = A * B^T * C0 style helpers
+template <int D>
+__device__ __forceinline__ void mmul(const double (&A)[D][D], const double (&B)[D][D], double (&C)[D][D]) {
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) s += A[i][k] * B[k][j];
+      C[i][j] = s;
+    }
+}
+template <int D>
+__device__ __forceinline__ void mmulT(const double (&A)[D][D], const double (&B)[D][D], double (&C)[D][D]) {
+  // C = A * B^T
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) s += A[i][k] * B[j][k];
+      C[i][j] = s;
+    }
+}
+
+// mu(T) given tau = det T, I1 = |T|^2 and (for non-template metrics) S.
+template <int D>
+__device__ __forceinline__ double metric_mu(int metric, double tau, double I1, const double (&S)[D][D]) {
+  switch (metric) {
+    case MU2: return I1 / (2.0 * tau) - 1.0;
+    case MU55: { double t = tau - 1.0; return t * t; }
+    case MU303: return I1 / (3.0 * cbrt(tau * tau)) - 1.0;
+    case MU7: return I1 + mfro2<D>(S) - 2.0 * D;
+    case MU302: return I1 * mfro2<D>(S) / 9.0 - 1.0;
+    default: /* MU321 */ return I1 + mfro2<D>(S) - 2.0 * D;
+  }
+}
+
+// (a_t, a_s): dmu/dT = a_t T + a_s S  (metrics.py:188-196, _kernels.py:89-98)
+__device__ __forceinline__ void metric_first_coeffs(int metric, double tau, double I1, double &at, double &as) {
+  switch (metric) {
+    case MU2: at = 1.0 / tau; as = -I1 / (2.0 * tau); break;
+    case MU55: at = 0.0; as = 2.0 * tau * (tau - 1.0); break;
+    case MU7: { double it2 = 1.0 / (tau * tau); at = 2.0 * (1.0 + it2); as = -2.0 * I1 * it2; } break;
+    default: /* MU303 */ {
+      double r = 1.0 / cbrt(tau * tau);
+      at = (2.0 / 3.0) * r; as = -(2.0 / 9.0) * I1 * r;
+    }
+  }
+}
+
+// (c_id, c_ts, c_ss, c_x) of the Hessian template (metrics.py:199-210,
+// _kernels.py:155-171); mu_7 derived in DESIGN.md.
+__device__ __forceinline__ void metric_second_coeffs(int metric, double tau, double I1, double (&c)[4]) {
+  switch (metric) {
+    case MU2: { double h = I1 / (2.0 * tau); c[0] = 1.0 / tau; c[1] = -1.0 / tau; c[2] = h; c[3] = h; } break;
+    case MU55: c[0] = 0.0; c[1] = 0.0; c[2] = 2.0 * tau * (2.0 * tau - 1.0); c[3] = -2.0 * tau * (tau - 1.0); break;
+    case MU7: { double it2 = 1.0 / (tau * tau);
+      c[0] = 2.0 * (1.0 + it2); c[1] = -4.0 * it2; c[2] = 4.0 * I1 * it2; c[3] = 2.0 * I1 * it2; } break;
+    default: /* MU303 */ {
+      double r = 1.0 / cbrt(tau * tau);
+      c[0] = (2.0 / 3.0) * r; c[1] = -(4.0 / 9.0) * r;
+      c[2] = (4.0 / 27.0) * I1 * r; c[3] = (2.0 / 9.0) * I1 * r;
+    }
+  }
+}
+
+// z = H g for the template block  c0 I + c1 (S(x)T + T(x)S) + c2 S(x)S + c3 S_mp S_on
+// (_kernels.py:235-258).
+template <int D>
+__device__ __forceinline__ void hess_template(const double (&c)[4], const double (&S)[D][D], const double (&T)[D][D],
+                                              const double (&g)[D][D], double (&z)[D][D]) {
+  const double dt = mdot<D>(T, g);
+  const double ds = mdot<D>(S, g);
+  const double w1 = c[1] * dt + c[2] * ds;
+  const double w2 = c[1] * ds;
+  // gs[p][n] = sum_o g[o][p] S[o][n] ; cross[a][n] = sum_p S[a][p] gs[p][n]
+  double gs[D][D];
+#pragma unroll
+  for (int p = 0; p < D; ++p)
+#pragma unroll
+    for (int n = 0; n < D; ++n) {
+      double s = 0.0;
+#pragma unroll
+      for (int o = 0; o < D; ++o) s += g[o][p] * S[o][n];
+      gs[p][n] = s;
+    }
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int n = 0; n < D; ++n) {
+      double cross = 0.0;
+#pragma unroll
+      for (int p = 0; p < D; ++p) cross += S[a][p] * gs[p][n];
+      z[a][n] = c[0] * g[a][n] + w1 * S[a][n] + w2 * T[a][n] + c[3] * cross;
+    }
+}
+
+// Non-template metrics (mu_302, mu_321): first derivative and Hessian action
+// from T and S = T^{-T}.  With I1 = |T|^2, J = |S|^2, M = S S^T S:
+//   dJ/dT = -2 M,  dS[g] = -S g^T S,  dM[g] = dS S^T S + S dS^T S + S S^T dS.
+//   mu_321 = I1 + J - 6:      P = 2T - 2M;              H g = 2g - 2 dM[g]
+//   mu_302 = I1 J / 9 - 1:    P = (2 J T - 2 I1 M)/9;
+//       H g = (2 dJ T + 2 J g - 2 dI1 M - 2 I1 dM[g]) / 9, dJ = -2 M:g, dI1 = 2 T:g
+template <int D>
+__device__ __forceinline__ void nt_first(int metric, const double (&T)[D][D], const double (&S)[D][D], double (&P)[D][D]) {
+  double SSt[D][D], M[D][D];
+  mmulT<D>(S, S, SSt);
+  mmul<D>(SSt, S, M);
+  if (metric == MU302) {
+    const double I1 = mfro2<D>(T), J = mfro2<D>(S);
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) P[i][j] = (2.0 * J * T[i][j] - 2.0 * I1 * M[i][j]) / 9.0;
+  } else {
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) P[i][j] = 2.0 * T[i][j] - 2.0 * M[i][j];
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void nt_hess(int metric, double w, const double (&S)[D][D], const double (&T)[D][D],
+                                        const double (&g)[D][D], double (&z)[D][D]) {
+  double SSt[D][D], M[D][D], dS[D][D], tmp[D][D], dM[D][D];
+  mmulT<D>(S, S, SSt);           // S S^T
+  mmul<D>(SSt, S, M);            // M = S S^T S
+  // dS = -S g^T S
+  mmulT<D>(S, g, tmp);           // S g^T
+  mmul<D>(tmp, S, dS);
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) dS[i][j] = -dS[i][j];
+  // dM = dS (S^T S) + S dS^T S + (S S^T) dS
+  double StS[D][D];
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) s += S[k][i] * S[k][j];
+      StS[i][j] = s;
+    }
+  double a1[D][D], a2[D][D], a3[D][D];
+  mmul<D>(dS, StS, a1);
+  mmulT<D>(S, dS, tmp);          // S dS^T
+  mmul<D>(tmp, S, a2);
+  mmul<D>(SSt, dS, a3);
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) dM[i][j] = a1[i][j] + a2[i][j] + a3[i][j];
+  if (metric == MU302) {
+    const double I1 = mfro2<D>(T), J = mfro2<D>(S);
+    const double dJ = -2.0 * mdot<D>(M, g), dI1 = 2.0 * mdot<D>(T, g);
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+        z[i][j] = w * ((2.0 * dJ * T[i][j] + 2.0 * J * g[i][j] - 2.0 * dI1 * M[i][j] - 2.0 * I1 * dM[i][j]) / 9.0);
+  } else {
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) z[i][j] = w * (2.0 * g[i][j] - 2.0 * dM[i][j]);
+  }
+}
+
+// ------------------------------------------------ deterministic reductions
+struct MinLoc {
+  double v;
+  int64_t i;
+};
+__device__ __forceinline__ MinLoc minloc(MinLoc a, MinLoc b) {
+  if (b.v < a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+
+// Fixed-order block reduction (warp shuffles in a fixed butterfly, then a
+// fixed pass over warp results).  Result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) r += scratch[w];
+  }
+  return r;
+}
+
+template <int NT>
+__device__ __forceinline__ MinLoc block_minloc(MinLoc m, double *sv, int64_t *si) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    MinLoc other;
+    other.v = __shfl_down_sync(0xffffffffu, m.v, o);
+    other.i = __shfl_down_sync(0xffffffffu, m.i, o);
+    m = minloc(m, other);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) { sv[wid] = m.v; si[wid] = m.i; }
+  __syncthreads();
+  MinLoc r{sv[0], si[0]};
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < NT / 32; ++w) r = minloc(r, MinLoc{sv[w], si[w]});
+  }
+  return r;
+}
+
+}  // namespace tmop

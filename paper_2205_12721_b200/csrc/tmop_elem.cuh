@@ -1,0 +1,738 @@
+// tmop_elem.cuh -- element kernels of the TMOP operator (one template for
+// every per-element entry point, specialised by KIND at compile time).
+//
+// A CTA owns EPB elements at a time and walks element groups with a
+// grid-stride loop (grid = min(#groups, GRID_CAP): a fixed function of the
+// mesh size, so every reduction below is bitwise reproducible run to run).
+// Per group:
+//   gather   restriction -> shared memory (coalesced index reads; nodal
+//            values come through L2, neighbours share nodes)
+//   forward  3 (2D: 2) sum-factorised 1D sweeps, B/G from the constant bank,
+//            z axis first like contract_dofs_to_quad (fe.py:227-239):
+//            X --z--> U(B,G) --y--> W(BB,BG,GB) --x--> grad[c][dir] at points
+//   point    KIND-specific quadrature-point work (setup / Hessian block /
+//            first derivative / energy / det)
+//   backward the transposed sweeps (fe.py:242-253), x axis first, with the
+//            three direction terms summed inside the sweeps, written as an
+//            element-blocked E-vector E[e][c][local]
+// The E-vector is summed to nodes by e2l_kernel in ascending element
+// order (np.add.at order, fe.py:189-204) -- no atomics anywhere.
+#pragma once
+
+#include <cfloat>
+#include <climits>
+
+#include "tmop_device.cuh"
+
+namespace tmop {
+
+enum Kind : int {
+  K_SETUP = 0,    // hessian_setup        (operator.py:350-371)
+  K_APPLY = 1,    // hessian_apply        (operator.py:401-418)
+  K_GRAD = 2,     // gradient             (operator.py:328-346)
+  K_ENERGY = 3,   // objective            (operator.py:311-326)
+  K_MINDET = 4,   // min_det_jacobian     (operator.py:296-304)
+  K_ELEMDET = 5,  // per-element min det  (operator.py:267-272 diagnostics)
+  K_VOLUME = 6,   // mesh_volume          (metrics.py:319-330)
+  K_DIAG = 7,     // hessian_diagonal     (operator.py:420-459)
+  K_APPLY_NT = 8, // hessian_apply, non-template metrics (mu_302 / mu_321)
+  K_DIAG_NT = 9,  // hessian_diagonal, non-template metrics
+  K_COUNT = 10
+};
+
+constexpr int GRID_CAP = 148 * 8;
+constexpr int ELEM_NT = 256;
+
+__host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int cclamp(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+template <int DIM, int N, int Q>
+struct Cfg {
+  static constexpr int NP = ipow(N, DIM);
+  static constexpr int QP = ipow(Q, DIM);
+  // 3D: R1 holds X / W / A (and det scratch); R2 holds U / grad+z / Bv.
+  // 2D: R1 holds X / grad+z (and diag x-sweep); R2 holds U / A (and diag points).
+  static constexpr int R1 = DIM == 3 ? cmax(cmax(3 * NP, 9 * Q * Q * N), QP) : cmax(cmax(2 * NP, 4 * QP), 2 * Q * N);
+  static constexpr int R2 = DIM == 3 ? cmax(6 * Q * N * N, 9 * QP) : cmax(4 * Q * N, 2 * QP);
+  static constexpr int PER = R1 + R2;
+  static constexpr int EPB = cclamp(8192 / PER, 1, 32);  // ~64 KB of shared memory per CTA
+  static constexpr int SMEM = EPB * PER * 8;
+};
+
+struct ElemArgs {
+  int64_t ne, nn, ngroups;
+  const int32_t *__restrict__ restr;
+  const uint8_t *__restrict__ fixed;
+  const double *__restrict__ in;      // x (positions) or v (direction), T-vector
+  const double *__restrict__ qdata;   // K_APPLY / K_DIAG input
+  double *__restrict__ qout;          // K_SETUP output
+  double *__restrict__ E;             // K_APPLY / K_GRAD / K_DIAG E-vector output
+  double *__restrict__ part_sum;      // per-CTA partial sums (energy / volume)
+  double *__restrict__ part_min;      // per-CTA partial min det
+  int64_t *__restrict__ part_arg;
+  double *__restrict__ elem_min;      // K_ELEMDET
+  int32_t *__restrict__ elem_arg;
+  int metric;
+  double inv_s;       // 1 / target scale
+  double inv_s_dm1;   // inv_s^(d-1)
+  double inv_s_d;     // inv_s^d
+  double coef_e;      // omega * det_w               (operator.py:314)
+  double coef_g;      // omega * det_w * inv_s       (operator.py:330)
+  double coef_h;      // omega * det_w * inv_s^2     (operator.py:358-359)
+};
+
+// ------------------------------------------------------------- gather
+template <int DIM, int N, int Q, int C, bool MASK>
+__device__ __forceinline__ void gather(const ElemArgs &a, int64_t e0, double *R1) {
+  using CF = Cfg<DIM, N, Q>;
+  constexpr int NP = CF::NP, ITEMS = C * NP;
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+    const int e = w / ITEMS, r = w % ITEMS, c = r / NP, l = r % NP;
+    const int64_t eg = e0 + e;
+    double val = 0.0;
+    if (eg < a.ne) {
+      const int node = __ldg(a.restr + eg * NP + l);
+      val = __ldg(a.in + c * a.nn + node);
+      if (MASK && ((__ldg(a.fixed + node) >> c) & 1)) val = 0.0;
+    }
+    R1[e * CF::R1 + c * NP + l] = val;
+  }
+}
+
+// --------------------------------------------------------- 3D forward
+// X[c][kz][ky][kx] (R1) -> U[c][v][qz][ky][kx] (R2), v in {B, G}
+template <int N, int Q, int C>
+__device__ __forceinline__ void f1_3d(const Tab &t, const double *R1, double *R2) {
+  using CF = Cfg<3, N, Q>;
+  constexpr int ITEMS = C * N * N;
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+    const int e = w / ITEMS, r = w % ITEMS, c = r / (N * N), kk = r % (N * N);
+    const double *x = R1 + e * CF::R1 + c * N * N * N + kk;
+    double xv[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) xv[k] = x[k * N * N];
+    double *u = R2 + e * CF::R2 + c * 2 * Q * N * N + kk;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      double sb = 0.0, sg = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        sb += tB<Q, N>(t, q, k) * xv[k];
+        sg += tG<Q, N>(t, q, k) * xv[k];
+      }
+      u[q * N * N] = sb;
+      u[Q * N * N + q * N * N] = sg;
+    }
+  }
+}
+
+// U (R2) -> W[c][v3][qz][qy][kx] (R1), v3 in {BB, BG, GB} (z-table, y-table)
+template <int N, int Q, int C>
+__device__ __forceinline__ void f2_3d(const Tab &t, const double *R2, double *R1) {
+  using CF = Cfg<3, N, Q>;
+  constexpr int ITEMS = C * Q * N;
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+    const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * N), r2 = r % (Q * N), qz = r2 / N, kx = r2 % N;
+    const double *ub = R2 + e * CF::R2 + (c * 2 + 0) * Q * N * N + qz * N * N + kx;
+    const double *ug = ub + Q * N * N;
+    double vb[N], vg[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) { vb[k] = ub[k * N]; vg[k] = ug[k * N]; }
+    double *wb = R1 + e * CF::R1 + (c * 3) * Q * Q * N + qz * Q * N + kx;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        s0 += tB<Q, N>(t, q, k) * vb[k];
+        s1 += tG<Q, N>(t, q, k) * vb[k];
+        s2 += tB<Q, N>(t, q, k) * vg[k];
+      }
+      wb[q * N] = s0;
+      wb[Q * Q * N + q * N] = s1;
+      wb[2 * Q * Q * N + q * N] = s2;
+    }
+  }
+}
+
+// W (R1) -> grad[c*3+dir][qz][qy][qx] (R2); dir 0 = d/dx (G on x), 1 = d/dy, 2 = d/dz
+template <int N, int Q, int C>
+__device__ __forceinline__ void f3_3d(const Tab &t, const double *R1, double *R2) {
+  using CF = Cfg<3, N, Q>;
+  constexpr int ITEMS = C * Q * Q, QP = Q * Q * Q;
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+    const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * Q), qq = r % (Q * Q);
+    const double *wb = R1 + e * CF::R1 + (c * 3) * Q * Q * N + qq * N;
+    double bb[N], bg[N], gb[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      bb[k] = wb[k];
+      bg[k] = wb[Q * Q * N + k];
+      gb[k] = wb[2 * Q * Q * N + k];
+    }
+    double *g = R2 + e * CF::R2 + (c * 3) * QP + qq * Q;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        s0 += tG<Q, N>(t, q, k) * bb[k];
+        s1 += tB<Q, N>(t, q, k) * bg[k];
+        s2 += tB<Q, N>(t, q, k) * gb[k];
+      }
+      g[q] = s0;
+      g[QP + q] = s1;
+      g[2 * QP + q] = s2;
+    }
+  }
+}
+
+// -------------------------------------------------------- 3D backward
+// z[c*3+dir][q] (R2) -> A[c][v3][qz][qy][kx] (R1): A0 = Gx^T z0, A1 = Bx^T z1, A2 = Bx^T z2
+template <int N, int Q>
+__device__ __forceinline__ void b3_3d(const Tab &t, const double *R2, double *R1) {
+  using CF = Cfg<3, N, Q>;
+  constexpr int ITEMS = 3 * Q * Q, QP = Q * Q * Q;
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+    const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * Q), qq = r % (Q * Q);
+    const double *z = R2 + e * CF::R2 + (c * 3) * QP + qq * Q;
+    double z0[Q], z1[Q], z2[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) { z0[q] = z[q]; z1[q] = z[QP + q]; z2[q] = z[2 * QP + q]; }
+    double *A = R1 + e * CF::R1 + (c * 3) * Q * Q * N + qq * N;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        s0 += tG<Q, N>(t, q, k) * z0[q];
+        s1 += tB<Q, N>(t, q, k) * z1[q];
+        s2 += tB<Q, N>(t, q, k) * z2[q];
+      }
+      A[k] = s0;
+      A[Q * Q * N + k] = s1;
+      A[2 * Q * Q * N + k] = s2;
+    }
+  }
+}
+
+// A (R1) -> Bv[c][2][qz][ky][kx] (R2): b0 = By^T A0 + Gy^T A1, b1 = By^T A2
+template <int N, int Q>
+__device__ __forceinline__ void b2_3d(const Tab &t, const double *R1, double *R2) {
+  using CF = Cfg<3, N, Q>;
+  constexpr int ITEMS = 3 * Q * N;
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+    const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * N), r2 = r % (Q * N), qz = r2 / N, kx = r2 % N;
+    const double *A = R1 + e * CF::R1 + (c * 3) * Q * Q * N + qz * Q * N + kx;
+    double a0[Q], a1[Q], a2[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      a0[q] = A[q * N];
+      a1[q] = A[Q * Q * N + q * N];
+      a2[q] = A[2 * Q * Q * N + q * N];
+    }
+    double *b = R2 + e * CF::R2 + (c * 2) * Q * N * N + qz * N * N + kx;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        s0 += tB<Q, N>(t, q, k) * a0[q] + tG<Q, N>(t, q, k) * a1[q];
+        s1 += tB<Q, N>(t, q, k) * a2[q];
+      }
+      b[k * N] = s0;
+      b[Q * N * N + k * N] = s1;
+    }
+  }
+}
+
+// Bv (R2) -> E[e][c][kz][ky][kx] (global) = Bz^T b0 + Gz^T b1
+template <int N, int Q>
+__device__ __forceinline__ void b1_3d(const Tab &t, const double *R2, double *__restrict__ E, int64_t e0,
+                                      int64_t ne) {
+  using CF = Cfg<3, N, Q>;
+  constexpr int ITEMS = 3 * N * N, NP = N * N * N;
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+    const int e = w / ITEMS, r = w % ITEMS, c = r / (N * N), kk = r % (N * N);
+    if (e0 + e >= ne) continue;
+    const double *b = R2 + e * CF::R2 + (c * 2) * Q * N * N + kk;
+    double b0[Q], b1[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) { b0[q] = b[q * N * N]; b1[q] = b[Q * N * N + q * N * N]; }
+    double *out = E + ((e0 + e) * 3 + c) * NP + kk;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) s += tB<Q, N>(t, q, k) * b0[q] + tG<Q, N>(t, q, k) * b1[q];
+      out[k * N * N] = s;
+    }
+  }
+}
+
+// --------------------------------------------------------- 2D sweeps
+// X[c][ky][kx] (R1) -> U[c][v][qy][kx] (R2)
+template <int N, int Q, int C>
+__device__ __forceinline__ void f1_2d(const Tab &t, const double *R1, double *R2) {
+  using CF = Cfg<2, N, Q>;
+  constexpr int ITEMS = C * N;
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+    const int e = w / ITEMS, r = w % ITEMS, c = r / N, kx = r % N;
+    const double *x = R1 + e * CF::R1 + c * N * N + kx;
+    double xv[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) xv[k] = x[k * N];
+    double *u = R2 + e * CF::R2 + c * 2 * Q * N + kx;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      double sb = 0.0, sg = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        sb += tB<Q, N>(t, q, k) * xv[k];
+        sg += tG<Q, N>(t, q, k) * xv[k];
+      }
+      u[q * N] = sb;
+      u[Q * N + q * N] = sg;
+    }
+  }
+}
+
+// U (R2) -> grad[c*2+dir][qy][qx] (R1 is free; we write to R2 after a copy?)
+// To keep the ping-pong simple in 2D: U lives in R2, grad is written to R1.
+template <int N, int Q, int C>
+__device__ __forceinline__ void f2_2d(const Tab &t, const double *R2, double *G) {
+  using CF = Cfg<2, N, Q>;
+  constexpr int ITEMS = C * Q, QP = Q * Q;
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+    const int e = w / ITEMS, r = w % ITEMS, c = r / Q, qy = r % Q;
+    const double *ub = R2 + e * CF::R2 + (c * 2) * Q * N + qy * N;
+    const double *ug = ub + Q * N;
+    double vb[N], vg[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) { vb[k] = ub[k]; vg[k] = ug[k]; }
+    double *g = G + e * CF::R1 + (c * 2) * QP + qy * Q;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        s0 += tG<Q, N>(t, q, k) * vb[k];
+        s1 += tB<Q, N>(t, q, k) * vg[k];
+      }
+      g[q] = s0;
+      g[QP + q] = s1;
+    }
+  }
+}
+
+// z[c*2+dir][q] (R1) -> A[c][v][qy][kx] (R2): A0 = Gx^T z0, A1 = Bx^T z1
+template <int N, int Q>
+__device__ __forceinline__ void b2_2d(const Tab &t, const double *Z, double *R2) {
+  using CF = Cfg<2, N, Q>;
+  constexpr int ITEMS = 2 * Q, QP = Q * Q;
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+    const int e = w / ITEMS, r = w % ITEMS, c = r / Q, qy = r % Q;
+    const double *z = Z + e * CF::R1 + (c * 2) * QP + qy * Q;
+    double z0[Q], z1[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) { z0[q] = z[q]; z1[q] = z[QP + q]; }
+    double *A = R2 + e * CF::R2 + (c * 2) * Q * N + qy * N;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        s0 += tG<Q, N>(t, q, k) * z0[q];
+        s1 += tB<Q, N>(t, q, k) * z1[q];
+      }
+      A[k] = s0;
+      A[Q * N + k] = s1;
+    }
+  }
+}
+
+// A (R2) -> E[e][c][ky][kx] = By^T A0 + Gy^T A1
+template <int N, int Q>
+__device__ __forceinline__ void b1_2d(const Tab &t, const double *R2, double *__restrict__ E, int64_t e0,
+                                      int64_t ne) {
+  using CF = Cfg<2, N, Q>;
+  constexpr int ITEMS = 2 * N, NP = N * N;
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+    const int e = w / ITEMS, r = w % ITEMS, c = r / N, kx = r % N;
+    if (e0 + e >= ne) continue;
+    const double *A = R2 + e * CF::R2 + (c * 2) * Q * N + kx;
+    double a0[Q], a1[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) { a0[q] = A[q * N]; a1[q] = A[Q * N + q * N]; }
+    double *out = E + ((e0 + e) * 2 + c) * NP + kx;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) s += tB<Q, N>(t, q, k) * a0[q] + tG<Q, N>(t, q, k) * a1[q];
+      out[k * N] = s;
+    }
+  }
+}
+
+// ------------------------------------------------ point-level helpers
+template <int D>
+__device__ __forceinline__ void load_point(const double *g, int stride, double (&A)[D][D]) {
+#pragma unroll
+  for (int c = 0; c < D; ++c)
+#pragma unroll
+    for (int d = 0; d < D; ++d) A[c][d] = g[(c * D + d) * stride];
+}
+template <int D>
+__device__ __forceinline__ void store_point(double *g, int stride, const double (&A)[D][D]) {
+#pragma unroll
+  for (int c = 0; c < D; ++c)
+#pragma unroll
+    for (int d = 0; d < D; ++d) g[(c * D + d) * stride] = A[c][d];
+}
+
+template <int D>
+__host__ __device__ constexpr int qfields_template() { return 4 + 2 * D * D; }
+template <int D>
+__host__ __device__ constexpr int qfields_nt() { return 1 + 2 * D * D; }
+
+// ------------------------------------------------------ the kernel
+template <int DIM, int N, int Q, int KIND>
+__global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
+  using CF = Cfg<DIM, N, Q>;
+  constexpr int QP = CF::QP, EPB = CF::EPB;
+  extern __shared__ double smem[];
+  double *R1 = smem;
+  double *R2 = smem + EPB * CF::R1;
+  __shared__ double red_v[ELEM_NT / 32];
+  __shared__ int64_t red_i[ELEM_NT / 32];
+
+  // The Hessian-action kernels are specialised per metric family so the
+  // template path does not carry the register footprint of the mu_302/321 one.
+  const bool tmpl = (KIND == K_APPLY) ? true : (KIND == K_APPLY_NT ? false : metric_is_template(a.metric));
+  double acc = 0.0;
+  MinLoc mn{DBL_MAX, LLONG_MAX};
+
+  for (int64_t grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
+    const int64_t e0 = grp * EPB;
+    gather<DIM, N, Q, DIM, KIND == K_APPLY || KIND == K_APPLY_NT>(a, e0, R1);
+    __syncthreads();
+    // ---- forward: gradients of the gathered field at the points
+    double *Gp;  // grad[c*DIM+dir][q] per element, stride R?
+    int gstride;
+    if constexpr (DIM == 3) {
+      f1_3d<N, Q, 3>(t, R1, R2);
+      __syncthreads();
+      f2_3d<N, Q, 3>(t, R2, R1);
+      __syncthreads();
+      f3_3d<N, Q, 3>(t, R1, R2);
+      Gp = R2;
+      gstride = CF::R2;
+    } else {
+      f1_2d<N, Q, 2>(t, R1, R2);
+      __syncthreads();
+      f2_2d<N, Q, 2>(t, R2, R1);
+      Gp = R1;
+      gstride = CF::R1;
+    }
+    __syncthreads();
+
+    // ---- point stage
+    for (int w = threadIdx.x; w < EPB * QP; w += ELEM_NT) {
+      const int e = w / QP, q = w % QP;
+      const int64_t eg = e0 + e;
+      if (eg >= a.ne) continue;
+      double *gp = Gp + e * gstride + q;
+      double A[DIM][DIM];
+      load_point<DIM>(gp, QP, A);
+
+      if constexpr (KIND == K_APPLY || KIND == K_APPLY_NT) {
+        double z[DIM][DIM];
+        if constexpr (KIND == K_APPLY) {
+          constexpr int F = qfields_template<DIM>();
+          const double *qd = a.qdata + eg * F * QP + q;
+          double c[4], S[DIM][DIM], T[DIM][DIM];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) c[k] = __ldg(qd + k * QP);
+          load_point<DIM>(qd + 4 * QP, QP, S);
+          load_point<DIM>(qd + (4 + DIM * DIM) * QP, QP, T);
+          hess_template<DIM>(c, S, T, A, z);
+        } else {
+          constexpr int F = qfields_nt<DIM>();
+          const double *qd = a.qdata + eg * F * QP + q;
+          double S[DIM][DIM], T[DIM][DIM];
+          const double wv = __ldg(qd);
+          load_point<DIM>(qd + QP, QP, S);
+          load_point<DIM>(qd + (1 + DIM * DIM) * QP, QP, T);
+          nt_hess<DIM>(a.metric, wv, S, T, A, z);
+        }
+        store_point<DIM>(gp, QP, z);
+      } else {
+        // A is the Jacobian dx/dxi at the point
+        const double dj = mdet<DIM>(A);
+        if constexpr (KIND == K_VOLUME) {
+          acc += dj * wq<DIM, Q>(t, q);
+        } else if constexpr (KIND == K_ELEMDET) {
+          R1[e * CF::R1 + q] = dj;  // (2D: grad lives in R1 too, but per-point in place is safe)
+        } else {
+          mn = minloc(mn, MinLoc{dj, eg * QP + q});
+        }
+        if constexpr (KIND == K_SETUP || KIND == K_GRAD || KIND == K_ENERGY) {
+          const double tau = dj * a.inv_s_d;
+          const double I1 = mfro2<DIM>(A) * (a.inv_s * a.inv_s);
+          const double cs = a.inv_s_dm1 / tau;
+          double Cof[DIM][DIM];
+          mcof<DIM>(A, Cof);
+          double S[DIM][DIM], T[DIM][DIM];
+#pragma unroll
+          for (int i = 0; i < DIM; ++i)
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) {
+              S[i][j] = cs * Cof[i][j];
+              T[i][j] = a.inv_s * A[i][j];
+            }
+          const double wpt = wq<DIM, Q>(t, q);
+          if constexpr (KIND == K_ENERGY) {
+            acc += wpt * metric_mu<DIM>(a.metric, tau, I1, S);
+          } else if constexpr (KIND == K_SETUP) {
+            if (tmpl) {
+              constexpr int F = qfields_template<DIM>();
+              double *qo = a.qout + eg * F * QP + q;
+              double c[4];
+              metric_second_coeffs(a.metric, tau, I1, c);
+              const double sw = a.coef_h * wpt;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) qo[k * QP] = sw * c[k];
+              store_point<DIM>(qo + 4 * QP, QP, S);
+              store_point<DIM>(qo + (4 + DIM * DIM) * QP, QP, T);
+            } else {
+              constexpr int F = qfields_nt<DIM>();
+              double *qo = a.qout + eg * F * QP + q;
+              qo[0] = a.coef_h * wpt;
+              store_point<DIM>(qo + QP, QP, S);
+              store_point<DIM>(qo + (1 + DIM * DIM) * QP, QP, T);
+            }
+          } else {  // K_GRAD
+            const double cw = a.coef_g * wpt;
+            double P[DIM][DIM];
+            if (tmpl) {
+              double at, as;
+              metric_first_coeffs(a.metric, tau, I1, at, as);
+              const double ct = cw * at * a.inv_s;
+              const double cc = cw * as * a.inv_s_dm1 / tau;
+#pragma unroll
+              for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                for (int j = 0; j < DIM; ++j) P[i][j] = ct * A[i][j] + cc * Cof[i][j];
+            } else {
+              nt_first<DIM>(a.metric, T, S, P);
+#pragma unroll
+              for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                for (int j = 0; j < DIM; ++j) P[i][j] *= cw;
+            }
+            store_point<DIM>(gp, QP, P);
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    if constexpr (KIND == K_ELEMDET) {
+      for (int e = threadIdx.x; e < EPB; e += ELEM_NT) {
+        const int64_t eg = e0 + e;
+        if (eg >= a.ne) continue;
+        double m = R1[e * CF::R1];
+        int arg = 0;
+        for (int q = 1; q < QP; ++q) {
+          const double v = R1[e * CF::R1 + q];
+          if (v < m) { m = v; arg = q; }
+        }
+        a.elem_min[eg] = m;
+        a.elem_arg[eg] = arg;
+      }
+      __syncthreads();
+    }
+
+    // ---- backward sweeps to the element-blocked E-vector
+    if constexpr (KIND == K_APPLY || KIND == K_APPLY_NT || KIND == K_GRAD) {
+      if constexpr (DIM == 3) {
+        b3_3d<N, Q>(t, R2, R1);
+        __syncthreads();
+        b2_3d<N, Q>(t, R1, R2);
+        __syncthreads();
+        b1_3d<N, Q>(t, R2, a.E, e0, a.ne);
+      } else {
+        b2_2d<N, Q>(t, R1, R2);
+        __syncthreads();
+        b1_2d<N, Q>(t, R2, a.E, e0, a.ne);
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- per-CTA deterministic partials
+  if constexpr (KIND == K_ENERGY || KIND == K_VOLUME) {
+    const double s = block_sum<ELEM_NT>(acc, red_v);
+    if (threadIdx.x == 0) a.part_sum[blockIdx.x] = s;
+  }
+  if constexpr (KIND == K_SETUP || KIND == K_GRAD || KIND == K_ENERGY || KIND == K_MINDET) {
+    const MinLoc m = block_minloc<ELEM_NT>(mn, red_v, red_i);
+    if (threadIdx.x == 0) {
+      a.part_min[blockIdx.x] = m.v;
+      a.part_arg[blockIdx.x] = m.i;
+    }
+  }
+}
+
+// ------------------------------------------------- diagonal (K_DIAG)
+// diag[(a,i)] = sum_q sum_{n,p} D_n(q,i) H[(a,n),(a,p)](q) D_p(q,i), with
+// D_n(q,i) D_p(q,i) a product of per-axis tables (Mn .* Mp) (operator.py:
+// 433-451).  One (n,p) pair at a time: point values -> 3 transposed sweeps,
+// accumulated into the E-vector.
+template <int Q, int N>
+__device__ __forceinline__ double tprod(const Tab &t, int sel, int q, int k) {
+  // sel: 0 = B.B, 1 = B.G, 2 = G.G
+  const double b = tB<Q, N>(t, q, k), g = tG<Q, N>(t, q, k);
+  return sel == 0 ? b * b : (sel == 1 ? b * g : g * g);
+}
+
+template <int DIM, int N, int Q, bool NTM>
+__global__ void __launch_bounds__(ELEM_NT) diag_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
+  using CF = Cfg<DIM, N, Q>;
+  constexpr int QP = CF::QP, NP = CF::NP, EPB = CF::EPB;
+  extern __shared__ double smem[];
+  double *R1 = smem;
+  double *R2 = smem + EPB * CF::R1;
+
+  for (int64_t grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
+    const int64_t e0 = grp * EPB;
+    for (int n = 0; n < DIM; ++n) {
+      for (int p = 0; p < DIM; ++p) {
+        // point values hv[c][q] -> R2
+        for (int w = threadIdx.x; w < EPB * QP; w += ELEM_NT) {
+          const int e = w / QP, q = w % QP;
+          const int64_t eg = e0 + e;
+          double hv[DIM];
+          if (eg < a.ne) {
+            if constexpr (!NTM) {
+              constexpr int F = qfields_template<DIM>();
+              const double *qd = a.qdata + eg * F * QP + q;
+              const double c0 = qd[0], c1 = qd[QP], c23 = qd[2 * QP] + qd[3 * QP];
+#pragma unroll
+              for (int c = 0; c < DIM; ++c) {
+                const double sn = qd[(4 + c * DIM + n) * QP], sp = qd[(4 + c * DIM + p) * QP];
+                const double tn = qd[(4 + DIM * DIM + c * DIM + n) * QP], tp = qd[(4 + DIM * DIM + c * DIM + p) * QP];
+                double v = c1 * (sn * tp + tn * sp) + c23 * sn * sp;
+                if (n == p) v += c0;
+                hv[c] = v;
+              }
+            } else {
+              constexpr int F = qfields_nt<DIM>();
+              const double *qd = a.qdata + eg * F * QP + q;
+              double S[DIM][DIM], T[DIM][DIM];
+              const double wv = qd[0];
+              load_point<DIM>(qd + QP, QP, S);
+              load_point<DIM>(qd + (1 + DIM * DIM) * QP, QP, T);
+#pragma unroll
+              for (int c = 0; c < DIM; ++c) {
+                double g[DIM][DIM] = {}, z[DIM][DIM];
+                g[c][p] = 1.0;
+                nt_hess<DIM>(a.metric, wv, S, T, g, z);
+                hv[c] = z[c][n];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) hv[c] = 0.0;
+          }
+#pragma unroll
+          for (int c = 0; c < DIM; ++c) R2[e * CF::R2 + c * QP + q] = hv[c];
+        }
+        __syncthreads();
+        // per-axis table selectors (axis 0 = x)
+        int sel[3];
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) sel[ax] = (ax == n) + (ax == p);
+        const bool first = (n == 0 && p == 0);
+        if constexpr (DIM == 3) {
+          // x: R2 [c][qz][qy][qx] -> R1 [c][qz][qy][kx]
+          for (int w = threadIdx.x; w < EPB * 3 * Q * Q; w += ELEM_NT) {
+            const int e = w / (3 * Q * Q), r = w % (3 * Q * Q);
+            const double *z = R2 + e * CF::R2 + r * Q;
+            double *o = R1 + e * CF::R1 + r * N;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              double s = 0.0;
+#pragma unroll
+              for (int q = 0; q < Q; ++q) s += tprod<Q, N>(t, sel[0], q, k) * z[q];
+              o[k] = s;
+            }
+          }
+          __syncthreads();
+          // y: R1 [c][qz][qy][kx] -> R2 [c][qz][ky][kx]
+          for (int w = threadIdx.x; w < EPB * 3 * Q * N; w += ELEM_NT) {
+            const int e = w / (3 * Q * N), r = w % (3 * Q * N), cz = r / N, kx = r % N;
+            const double *z = R1 + e * CF::R1 + cz * Q * N + kx;
+            double *o = R2 + e * CF::R2 + cz * N * N + kx;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              double s = 0.0;
+#pragma unroll
+              for (int q = 0; q < Q; ++q) s += tprod<Q, N>(t, sel[1], q, k) * z[q * N];
+              o[k * N] = s;
+            }
+          }
+          __syncthreads();
+          // z: R2 [c][qz][ky][kx] -> E [e][c][kz][ky][kx] (accumulate)
+          for (int w = threadIdx.x; w < EPB * 3 * N * N; w += ELEM_NT) {
+            const int e = w / (3 * N * N), r = w % (3 * N * N), c = r / (N * N), kk = r % (N * N);
+            if (e0 + e >= a.ne) continue;
+            const double *z = R2 + e * CF::R2 + c * Q * N * N + kk;
+            double *o = a.E + ((e0 + e) * 3 + c) * NP + kk;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              double s = 0.0;
+#pragma unroll
+              for (int q = 0; q < Q; ++q) s += tprod<Q, N>(t, sel[2], q, k) * z[q * N * N];
+              o[k * N * N] = first ? s : o[k * N * N] + s;
+            }
+          }
+        } else {
+          // x: R2 [c][qy][qx] -> R1 [c][qy][kx]
+          for (int w = threadIdx.x; w < EPB * 2 * Q; w += ELEM_NT) {
+            const int e = w / (2 * Q), r = w % (2 * Q);
+            const double *z = R2 + e * CF::R2 + r * Q;
+            double *o = R1 + e * CF::R1 + r * N;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              double s = 0.0;
+#pragma unroll
+              for (int q = 0; q < Q; ++q) s += tprod<Q, N>(t, sel[0], q, k) * z[q];
+              o[k] = s;
+            }
+          }
+          __syncthreads();
+          // y: R1 [c][qy][kx] -> E [e][c][ky][kx]
+          for (int w = threadIdx.x; w < EPB * 2 * N; w += ELEM_NT) {
+            const int e = w / (2 * N), r = w % (2 * N), c = r / N, kx = r % N;
+            if (e0 + e >= a.ne) continue;
+            const double *z = R1 + e * CF::R1 + c * Q * N + kx;
+            double *o = a.E + ((e0 + e) * 2 + c) * NP + kx;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              double s = 0.0;
+#pragma unroll
+              for (int q = 0; q < Q; ++q) s += tprod<Q, N>(t, sel[1], q, k) * z[q * N];
+              o[k * N] = first ? s : o[k * N] + s;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+}  // namespace tmop

@@ -1,0 +1,8 @@
+// Element-kernel instantiations: 3D hexes, p = 2 (n1 = 3), n_q = 2..9.
+#include "tmop_launch.cuh"
+
+namespace tmop {
+int launch_elem_3d_n3(int nq, int kind, ElemArgs &a, const Tab &t, cudaStream_t s) {
+  return launch_q<3, 3>(nq, kind, a, t, s);
+}
+}  // namespace tmop

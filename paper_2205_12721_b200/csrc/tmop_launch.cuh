@@ -1,0 +1,69 @@
+// tmop_launch.cuh -- compile-time dispatch of the element kernels over
+// (n_q, kind) for one (dim, p+1); included by one small .cu per (dim, p+1)
+// so the instantiations compile in parallel.
+#pragma once
+
+#include <algorithm>
+
+#include "tmop_elem.cuh"
+#include "tmop_internal.h"
+
+namespace tmop {
+
+template <int DIM, int N, int Q, int KIND>
+int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
+  using CF = Cfg<DIM, N, Q>;
+  a.ngroups = (a.ne + CF::EPB - 1) / CF::EPB;
+  const int grid = (int)std::min<int64_t>(a.ngroups, GRID_CAP);
+  if (grid == 0) return 0;
+  void (*kfn)(const ElemArgs, const Tab);
+  if constexpr (KIND == K_DIAG) {
+    kfn = diag_kernel<DIM, N, Q, false>;
+  } else if constexpr (KIND == K_DIAG_NT) {
+    kfn = diag_kernel<DIM, N, Q, true>;
+  } else {
+    kfn = elem_kernel<DIM, N, Q, KIND>;
+  }
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM) != cudaSuccess) return -2;
+    configured = true;
+  }
+  kfn<<<grid, ELEM_NT, CF::SMEM, s>>>(a, t);
+  return grid;
+}
+
+template <int DIM, int N, int Q>
+int launch_kind(int kind, ElemArgs &a, const Tab &t, cudaStream_t s) {
+  switch (kind) {
+    case K_SETUP: return launch_one<DIM, N, Q, K_SETUP>(a, t, s);
+    case K_APPLY: return launch_one<DIM, N, Q, K_APPLY>(a, t, s);
+    case K_GRAD: return launch_one<DIM, N, Q, K_GRAD>(a, t, s);
+    case K_ENERGY: return launch_one<DIM, N, Q, K_ENERGY>(a, t, s);
+    case K_MINDET: return launch_one<DIM, N, Q, K_MINDET>(a, t, s);
+    case K_ELEMDET: return launch_one<DIM, N, Q, K_ELEMDET>(a, t, s);
+    case K_VOLUME: return launch_one<DIM, N, Q, K_VOLUME>(a, t, s);
+    case K_DIAG: return launch_one<DIM, N, Q, K_DIAG>(a, t, s);
+    case K_APPLY_NT: return launch_one<DIM, N, Q, K_APPLY_NT>(a, t, s);
+    case K_DIAG_NT: return launch_one<DIM, N, Q, K_DIAG_NT>(a, t, s);
+    default: return -1;
+  }
+}
+
+// Supported n_q: 2..9 for every p.
+template <int DIM, int N>
+int launch_q(int nq, int kind, ElemArgs &a, const Tab &t, cudaStream_t s) {
+  switch (nq) {
+    case 2: return launch_kind<DIM, N, 2>(kind, a, t, s);
+    case 3: return launch_kind<DIM, N, 3>(kind, a, t, s);
+    case 4: return launch_kind<DIM, N, 4>(kind, a, t, s);
+    case 5: return launch_kind<DIM, N, 5>(kind, a, t, s);
+    case 6: return launch_kind<DIM, N, 6>(kind, a, t, s);
+    case 7: return launch_kind<DIM, N, 7>(kind, a, t, s);
+    case 8: return launch_kind<DIM, N, 8>(kind, a, t, s);
+    case 9: return launch_kind<DIM, N, 9>(kind, a, t, s);
+    default: return -1;
+  }
+}
+
+}  // namespace tmop

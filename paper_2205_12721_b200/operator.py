@@ -1,0 +1,382 @@
+"""Device TMOP operator: the reference `TmopProblem` API (operator.py:220-459)
+backed by the sm_100a kernels of libtmop_b200.so.
+
+Every method accepts numpy arrays or torch tensors.  numpy in -> numpy out
+(host buffers, explicit H2D / D2H copies: the drop-in path); torch CUDA in ->
+torch CUDA out (device-resident path used by the solvers).  There is no CPU
+implementation: without the library or a CUDA device every call raises.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .fe import Basis1D, OpCounter, build_eval_matrices, gauss_legendre_1d, tensor_weights
+from .mesh import Mesh
+from .metrics import (MetricId, TargetData, TargetSpec, build_targets, check_metric_dim,
+                      is_template_metric)
+
+__all__ = ["InvalidMeshError", "LimitingConfig", "ObjectiveConfig", "HessQData", "TmopProblem",
+           "DeviceMesh", "mesh_volume"]
+
+
+class InvalidMeshError(RuntimeError):
+    """Nonpositive Jacobian determinant at a quadrature point (operator.py:45-54)."""
+
+    def __init__(self, element: int, point: int, value: float):
+        self.element = element
+        self.point = point
+        self.value = value
+        super().__init__(f"nonpositive det(A) = {value:.3e} in element {element}, quadrature point {point}")
+
+
+@dataclass
+class LimitingConfig:
+    """Penalty |x - x0|^2 / delta^2 (operator.py:57-76)."""
+    reference: np.ndarray
+    delta: float | np.ndarray = 1.0
+    weight: float = 1.0
+
+    def validate(self, n_dofs: int) -> None:
+        if np.shape(self.reference) != (n_dofs,):
+            raise ValueError(f"limiting reference has shape {np.shape(self.reference)}, expected ({n_dofs},)")
+        if np.any(np.asarray(self.delta) <= 0):
+            raise ValueError("limiting delta must be positive everywhere")
+        if self.weight <= 0:
+            raise ValueError(f"limiting weight must be positive, got {self.weight}")
+
+
+@dataclass
+class ObjectiveConfig:
+    metric: MetricId
+    target: TargetSpec
+    spatial_weight: float = 1.0
+    limiting: LimitingConfig | None = None
+
+    def validate(self) -> None:
+        if self.spatial_weight <= 0:
+            raise ValueError(f"spatial weight must be positive, got {self.spatial_weight}")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class DeviceMesh:
+    """Mesh arrays resident in HBM: restriction (int32), per-node fixed flags
+    (uint8, bit a = component a constrained) and the L->E transpose map
+    (int64 offsets, uint32 E-indices e*Np+l sorted by node, then element) that
+    makes the E->L sum deterministic in np.add.at order (fe.py:189-204)."""
+
+    def __init__(self, mesh: Mesh, device):
+        torch = _torch()
+        self.device = device
+        self.n_nodes = mesh.n_nodes
+        self.n_elements = mesh.n_elements
+        restr = torch.from_numpy(np.ascontiguousarray(mesh.restriction, dtype=np.int32)).to(device)
+        self.restriction = restr
+        flags = np.zeros(mesh.n_nodes, dtype=np.uint8)
+        for a in range(mesh.dim):
+            flags |= (mesh.fixed_mask[a].astype(np.uint8) << a)
+        self.fixed = torch.from_numpy(flags).to(device)
+        self.fixed_mask = torch.from_numpy(np.ascontiguousarray(mesh.fixed_mask.ravel())).to(device)
+        flat = restr.reshape(-1).to(torch.int64)
+        order = torch.sort(flat, stable=True).indices   # ascending node, then ascending (e, l)
+        counts = torch.bincount(flat, minlength=mesh.n_nodes)
+        self.l2e_offsets = torch.zeros(mesh.n_nodes + 1, dtype=torch.int64, device=device)
+        self.l2e_offsets[1:] = torch.cumsum(counts, 0)
+        # uint32 storage (torch has no uint32 arithmetic needs here; int32 view
+        # is reinterpreted by the kernel)
+        self.l2e_index = order.to(torch.int32)
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+@dataclass
+class HessQData:
+    """Partially assembled Hessian on the device (operator.py:91-138).
+
+    `data` is element-blocked: (n_elements, fields, Q) float64 with fields =
+    c_id, c_ts, c_ss, c_x, S (d*d), T (d*d) for template metrics (the
+    reference's 4 + 2 d^2 values per point) and w, S, T for mu_302 / mu_321.
+    The reference's planar arrays are materialised on demand.
+    """
+    data: object
+    dim: int
+    n_quad_total: int
+    template: bool
+    host: bool = False   # built from a numpy x: diagonal() answers in numpy
+
+    @property
+    def nbytes(self) -> int:
+        return self.data.numel() * self.data.element_size()
+
+    @property
+    def n_elements(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def bytes_per_element(self) -> int:
+        return self.nbytes // max(self.n_elements, 1)
+
+    def _planar(self, lo: int, hi: int):
+        arr = self.data.permute(1, 0, 2).reshape(self.data.shape[1], -1).cpu().numpy()
+        return arr[lo:hi]
+
+    @property
+    def coeffs(self) -> np.ndarray:
+        if not self.template:
+            raise AttributeError("non-template metrics store (w, S, T) per point, not coeffs")
+        return self._planar(0, 4)
+
+    @property
+    def s_mat(self) -> np.ndarray:
+        o = 4 if self.template else 1
+        d = self.dim
+        return self._planar(o, o + d * d).reshape(d, d, -1)
+
+    @property
+    def t_mat(self) -> np.ndarray:
+        o = (4 if self.template else 1) + self.dim * self.dim
+        d = self.dim
+        return self._planar(o, o + d * d).reshape(d, d, -1)
+
+    def block(self, element: int, point: int) -> np.ndarray:
+        """Full (d^2 x d^2) block at (element, point) (operator.py:127-138)."""
+        if not self.template:
+            raise NotImplementedError("block() reconstruction is defined for template metrics")
+        d = self.dim
+        col = self.data[element, :, point].cpu().numpy()
+        c_id, c_ts, c_ss, c_x = col[:4]
+        sv = col[4:4 + d * d]
+        tv = col[4 + d * d:4 + 2 * d * d]
+        full = c_id * np.eye(d * d)
+        full += c_ts * (np.outer(sv, tv) + np.outer(tv, sv))
+        full += c_ss * np.outer(sv, sv)
+        s = sv.reshape(d, d)
+        full += c_x * np.einsum("mp,on->mnop", s, s).reshape(d * d, d * d)
+        return full
+
+
+class TmopProblem:
+    """Mesh + objective + quadrature on one GPU; the six `ProblemLike`
+    methods (solvers.py:183-189) run as sm_100a kernels.
+
+    `counter` accumulates the reference's multiply-add accounting
+    analytically; `batch_quad_points` only sets the element batching used to
+    report InvalidMeshError exactly like the reference (operator.py:267-272)
+    -- the kernels themselves stream all elements in one launch.
+    """
+
+    def __init__(self, mesh: Mesh, config: ObjectiveConfig, n_quad: int,
+                 counter: OpCounter | None = None, batch_quad_points: int = 2_000_000,
+                 device=None):
+        torch = _torch()
+        config.validate()
+        check_metric_dim(config.metric, mesh.dim)
+        if not torch.cuda.is_available():
+            raise _lib.TmopLibraryError("TmopProblem needs a CUDA device (sm_100a); none is available")
+        self.lib = _lib.load()
+        self.mesh = mesh
+        self.config = config
+        self.basis = Basis1D.gauss_lobatto(mesh.order)
+        self.rule = gauss_legendre_1d(n_quad)
+        self.em = build_eval_matrices(self.basis, self.rule)
+        self.wq = tensor_weights(self.rule, mesh.dim)
+        self.counter = counter
+        d = mesh.dim
+        self.n_quad = n_quad
+        self.n_quad_total = n_quad ** d
+        self._qshape = (n_quad,) * d
+        self.batch_elements = max(1, batch_quad_points // self.n_quad_total)
+        if config.limiting is not None:
+            config.limiting.validate(mesh.n_dofs)
+            raise NotImplementedError("the displacement-limiting term is not built yet on the device path")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.dmesh = DeviceMesh(mesh, self.device)
+        self._stream = None
+        ctx = _lib.C.c_void_p()
+        B = np.ascontiguousarray(self.em.b, dtype=np.float64)
+        G = np.ascontiguousarray(self.em.g, dtype=np.float64)
+        w1 = np.ascontiguousarray(self.rule.weights, dtype=np.float64)
+        dp = _lib.C.POINTER(_lib.C.c_double)
+        stream = torch.cuda.current_stream(self.device)
+        _lib.check(self.lib.tmop_ctx_create(
+            _lib.C.byref(ctx), d, mesh.order, n_quad, mesh.n_elements, mesh.n_nodes,
+            _lib.ptr(self.dmesh.restriction), _lib.ptr(self.dmesh.fixed), _lib.ptr(self.dmesh.l2e_offsets),
+            _lib.ptr(self.dmesh.l2e_index), B.ctypes.data_as(dp), G.ctypes.data_as(dp), w1.ctypes.data_as(dp),
+            int(config.metric), 1.0, 1.0, float(config.spatial_weight), stream.cuda_stream), "tmop_ctx_create")
+        self._ctx = ctx
+        self._stream = stream.cuda_stream
+        self._status = torch.zeros(2, dtype=torch.float64, device=self.device)
+        self._scalar = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.template = is_template_metric(config.metric)
+        self.qdata_fields = self.lib.tmop_qdata_fields(ctx)
+        if config.target.kind != 0 and config.target.h is None:
+            vol = self.volume(mesh.coords.ravel())
+            self.targets: TargetData = build_targets(mesh, config.target, self.rule, volume=vol)
+        else:
+            self.targets = build_targets(mesh, config.target, self.rule)
+        _lib.check(self.lib.tmop_ctx_set_target(ctx, self.targets.inv_scale, self.targets.det_w),
+                   "tmop_ctx_set_target")
+
+    def __del__(self):
+        ctx = getattr(self, "_ctx", None)
+        if ctx is not None and getattr(self, "lib", None) is not None:
+            self.lib.tmop_ctx_destroy(ctx)
+            self._ctx = None
+
+    # ------------------------------------------------------------ helpers
+    @property
+    def n_dofs(self) -> int:
+        return self.mesh.n_dofs
+
+    def _sync_stream(self):
+        torch = _torch()
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        if s != self._stream:
+            _lib.check(self.lib.tmop_ctx_set_stream(self._ctx, s), "tmop_ctx_set_stream")
+            self._stream = s
+
+    def _in(self, x):
+        """(device float64 contiguous tensor, came_from_numpy)."""
+        torch = _torch()
+        if _is_torch(x):
+            t = x.detach()
+            if t.device != self.device or t.dtype != torch.float64:
+                t = t.to(device=self.device, dtype=torch.float64)
+            t = t.reshape(-1).contiguous()
+            host = False
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64).reshape(-1)).to(self.device)
+            host = True
+        if t.numel() != self.mesh.n_dofs:
+            raise ValueError(f"expected a T-vector of length {self.mesh.n_dofs}, got {t.numel()}")
+        self._sync_stream()
+        return t, host
+
+    def _out(self, t, host):
+        return t.cpu().numpy() if host else t
+
+    def _det(self):
+        st = self._status.cpu().numpy()
+        return float(st[0]), int(st[1:2].view(np.int64)[0])
+
+    def _raise_if_inverted(self, x, min_det):
+        if min_det > 0.0:
+            return
+        # exact emulation of the reference's batched check (operator.py:267-272)
+        torch = _torch()
+        ne = self.mesh.n_elements
+        emin = torch.empty(ne, dtype=torch.float64, device=self.device)
+        earg = torch.empty(ne, dtype=torch.int32, device=self.device)
+        _lib.check(self.lib.tmop_element_min_det(self._ctx, _lib.ptr(x), _lib.ptr(emin), _lib.ptr(earg)),
+                   "tmop_element_min_det")
+        em = emin.cpu().numpy()
+        ea = earg.cpu().numpy()
+        for lo in range(0, ne, self.batch_elements):
+            hi = min(lo + self.batch_elements, ne)
+            k = int(np.argmin(em[lo:hi]))
+            if em[lo + k] <= 0.0:
+                raise InvalidMeshError(lo + k, int(ea[lo + k]), float(em[lo + k]))
+        raise InvalidMeshError(0, 0, min_det)
+
+    def _count(self, kind: str) -> None:
+        if self.counter is None:
+            return
+        d, n, q = self.mesh.dim, self.mesh.order + 1, self.n_quad
+        ne, Q = self.mesh.n_elements, self.n_quad_total
+        per_dir = sum(q ** k * n ** (d + 1 - k) for k in range(1, d + 1))
+        contr = d * d * per_dir * ne          # one d x d set of d-axis contractions
+        if kind == "apply":
+            self.counter.add(2 * contr + ne * Q * (6 * d * d + 2 * d ** 3))
+        elif kind in ("gradient",):
+            self.counter.add(2 * contr)
+        elif kind in ("setup", "objective", "min_det"):
+            self.counter.add(contr)
+
+    # ----------------------------------------------------------- ProblemLike
+    def volume(self, x) -> float:
+        xt, _ = self._in(x)
+        _lib.check(self.lib.tmop_volume(self._ctx, _lib.ptr(xt), _lib.ptr(self._scalar)), "tmop_volume")
+        return float(self._scalar.item())
+
+    def min_det_jacobian(self, x) -> float:
+        xt, _ = self._in(x)
+        _lib.check(self.lib.tmop_min_det(self._ctx, _lib.ptr(xt), _lib.ptr(self._status)), "tmop_min_det")
+        self._count("min_det")
+        return self._det()[0]
+
+    def objective(self, x) -> float:
+        """F(x); raises InvalidMeshError at the first nonpositive det(A)."""
+        xt, _ = self._in(x)
+        _lib.check(self.lib.tmop_objective(self._ctx, _lib.ptr(xt), _lib.ptr(self._scalar),
+                                           _lib.ptr(self._status)), "tmop_objective")
+        self._count("objective")
+        md, _ = self._det()
+        self._raise_if_inverted(xt, md)
+        return float(self._scalar.item())
+
+    def gradient(self, x, out=None):
+        torch = _torch()
+        xt, host = self._in(x)
+        g = torch.empty_like(xt) if out is None else out
+        _lib.check(self.lib.tmop_gradient(self._ctx, _lib.ptr(xt), _lib.ptr(g), _lib.ptr(self._status)),
+                   "tmop_gradient")
+        self._count("gradient")
+        md, _ = self._det()
+        self._raise_if_inverted(xt, md)
+        return self._out(g, host)
+
+    def hessian_setup(self, x) -> HessQData:
+        torch = _torch()
+        xt, host = self._in(x)
+        qd = torch.empty((self.mesh.n_elements, self.qdata_fields, self.n_quad_total), dtype=torch.float64,
+                         device=self.device)
+        _lib.check(self.lib.tmop_hessian_setup(self._ctx, _lib.ptr(xt), _lib.ptr(qd), _lib.ptr(self._status)),
+                   "tmop_hessian_setup")
+        self._count("setup")
+        md, _ = self._det()
+        self._raise_if_inverted(xt, md)
+        return HessQData(data=qd, dim=self.mesh.dim, n_quad_total=self.n_quad_total, template=self.template,
+                         host=host)
+
+    def hessian_apply(self, qdata: HessQData, v, out=None):
+        """Action of the Hessian frozen at the setup positions; constrained
+        inputs are treated as zero, constrained outputs return v
+        (operator.py:401-418)."""
+        torch = _torch()
+        vt, host = self._in(v)
+        y = torch.empty_like(vt) if out is None else out
+        _lib.check(self.lib.tmop_hessian_apply(self._ctx, _lib.ptr(qdata.data), _lib.ptr(vt), _lib.ptr(y)),
+                   "tmop_hessian_apply")
+        self._count("apply")
+        return self._out(y, host)
+
+    def hessian_diagonal(self, qdata: HessQData, out=None):
+        torch = _torch()
+        self._sync_stream()
+        y = torch.empty(self.mesh.n_dofs, dtype=torch.float64, device=self.device) if out is None else out
+        _lib.check(self.lib.tmop_hessian_diagonal(self._ctx, _lib.ptr(qdata.data), _lib.ptr(y)),
+                   "tmop_hessian_diagonal")
+        return self._out(y, qdata.host)
+
+    # ---------------------------------------------------------- raw C-ABI
+    @property
+    def ctx(self):
+        return self._ctx
+
+
+def mesh_volume(mesh: Mesh, rule, coords=None) -> float:
+    """Quadrature volume of the mesh image (metrics.py:319-330), on the GPU."""
+    from .metrics import MetricId, TargetKind, TargetSpec
+    metric = MetricId.MU_2 if mesh.dim == 2 else MetricId.MU_303
+    p = TmopProblem(mesh, ObjectiveConfig(metric, TargetSpec(TargetKind.IDEAL_UNIT)), rule.n_points)
+    x = mesh.coords.ravel() if coords is None else np.asarray(coords, dtype=float).ravel()
+    return p.volume(x)

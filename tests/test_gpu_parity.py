@@ -1,0 +1,221 @@
+"""GPU parity: the sm_100a kernels (through the C ABI, via the package API)
+against the reference's golden vectors and the CPU oracle.
+
+Tolerances (FP64): per-kernel outputs 1e-12 relative L2 (north_star); the
+reference's own PA/FA agreement is 1e-11 (tests/test_operator.py:152).
+Newton traces: alpha and MINRES iteration counts exact, F / |grad F| 1e-9,
+final x 1e-10 relative.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_names, load_golden
+from oracle import tmop_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def rel(a, b):
+    a = np.asarray(a.cpu() if hasattr(a, "cpu") else a, float)
+    b = np.asarray(b, float)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def make(g):
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(int(g["dim"]), tuple(int(c) for c in g["counts"]), int(g["order"]))
+    kind = P.TargetKind.IDEAL_UNIT if int(g["target"]) == 0 else P.TargetKind.IDEAL_EQUAL_SIZE
+    cfg = P.ObjectiveConfig(P.MetricId(int(g["metric"])), P.TargetSpec(kind),
+                            spatial_weight=float(g["spatial_weight"]))
+    return P.TmopProblem(mesh, cfg, int(g["n_quad"]))
+
+
+OPS = [n for n in golden_names("op") if not n.endswith("_lim")]
+
+
+@pytest.mark.parametrize("name", OPS)
+def test_operator_matches_reference_golden(name):
+    g = load_golden(name)
+    p = make(g)
+    assert p.targets.inv_scale == pytest.approx(float(g["inv_scale"]), rel=1e-13)
+    x, v = g["x"], g["v"]
+    qd = p.hessian_setup(x)
+    assert rel(qd.coeffs, g["coeffs"]) <= TOL
+    assert rel(qd.s_mat, g["s_mat"]) <= TOL
+    assert rel(qd.t_mat, g["t_mat"]) <= TOL
+    assert rel(p.hessian_apply(qd, v), g["apply"]) <= TOL
+    assert rel(p.gradient(x), g["gradient"]) <= TOL
+    assert p.objective(x) == pytest.approx(float(g["objective"]), rel=TOL, abs=1e-14)
+    assert rel(p.hessian_diagonal(qd), g["diagonal"]) <= TOL
+    assert p.min_det_jacobian(x) == pytest.approx(float(g["min_det"]), rel=1e-14)
+    assert p.min_det_jacobian(p.mesh.dof_vector()) == pytest.approx(float(g["min_det_uniform"]), rel=1e-14)
+
+
+def test_storage_accounting_and_blocks():
+    g = load_golden("op3d_p2_q4_mu303")
+    p = make(g)
+    qd = p.hessian_setup(g["x"])
+    assert qd.nbytes == 22 * 64 * 8 * 8          # reference test_operator.py:133-138
+    assert qd.bytes_per_element == 22 * 64 * 8
+    from oracle.tmop_oracle import metric_second
+    T = g["t_mat"][:, :, 13]
+    want = metric_second(303, T) * g["wq"][13]
+    assert np.allclose(qd.block(0, 13), want, atol=1e-12 * np.abs(want).max())
+
+
+def test_torch_path_matches_numpy_path_and_is_deterministic():
+    import torch
+    g = load_golden("op3d_p3_q5_mu303")
+    p = make(g)
+    xd = torch.from_numpy(g["x"]).cuda()
+    vd = torch.from_numpy(g["v"]).cuda()
+    qd = p.hessian_setup(xd)
+    y1 = p.hessian_apply(qd, vd)
+    y2 = p.hessian_apply(qd, vd)
+    assert y1.is_cuda
+    assert torch.equal(y1, y2)                     # bitwise run-to-run (no atomics)
+    assert rel(y1, g["apply"]) <= TOL
+    f1, f2 = p.objective(xd), p.objective(xd)
+    assert f1 == f2
+
+
+@pytest.mark.parametrize("dim,order,nq,metric,counts", [
+    (3, 2, 4, O.MU_303, (5, 4, 3)), (3, 1, 3, O.MU_303, (7, 5, 4)), (3, 4, 6, O.MU_303, (3, 2, 2)),
+    (3, 2, 6, O.MU_303, (3, 3, 2)), (3, 3, 9, O.MU_55, (2, 2, 2)),
+    (3, 1, 3, O.MU_302, (4, 3, 3)), (3, 2, 4, O.MU_321, (3, 3, 3)), (3, 3, 5, O.MU_302, (2, 2, 3)),
+    (2, 2, 4, O.MU_7, (5, 4)), (2, 4, 6, O.MU_2, (3, 3)), (2, 1, 2, O.MU_55, (6, 5)),
+])
+def test_operator_matches_oracle(dim, order, nq, metric, counts, rng):
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(dim, counts, order)
+    om = O.box_mesh(dim, counts, order)
+    op = O.OracleProblem(om, metric, nq)
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId(metric), P.TargetSpec(P.TargetKind.IDEAL_UNIT)), nq)
+    x = O.perturb(om, rng, 0.2)
+    v = rng.standard_normal(x.shape)
+    qd = p.hessian_setup(x)
+    oqd = op.hessian_setup(x)
+    assert rel(p.hessian_apply(qd, v), op.hessian_apply(oqd, v)) <= TOL
+    assert rel(p.gradient(x), op.gradient(x)) <= TOL
+    assert p.objective(x) == pytest.approx(op.objective(x), rel=TOL)
+    assert rel(p.hessian_diagonal(qd), op.hessian_diagonal(oqd)) <= TOL
+    assert p.min_det_jacobian(x) == pytest.approx(op.min_det_jacobian(x), rel=1e-14)
+
+
+def test_metric_points_match_reference():
+    import paper_2205_12721_b200 as P
+    g = load_golden("metric_points")
+    for metric, dim in [(2, 2), (55, 2), (55, 3), (303, 3)]:
+        T = g[f"T_{metric}_{dim}"]
+        assert rel(P.metric_value(metric, T), g[f"mu_{metric}_{dim}"]) <= 1e-13
+        assert rel(P.metric_first_derivative(metric, T), g[f"P_{metric}_{dim}"]) <= 1e-13
+        assert rel(P.metric_second_derivative(metric, T), g[f"H_{metric}_{dim}"]) <= 1e-13
+    rng = np.random.default_rng(3)
+    for metric, dim in [(7, 2), (302, 3), (321, 3)]:
+        T = np.stack([np.eye(dim) + 0.3 * rng.standard_normal((dim, dim)) for _ in range(20)])
+        T = T[np.linalg.det(T) > 0.1]
+        assert rel(P.metric_value(metric, T), O.metric_value(metric, T)) <= 1e-13
+        assert rel(P.metric_first_derivative(metric, T), O.metric_first(metric, T)) <= 1e-13
+        assert rel(P.metric_second_derivative(metric, T), O.metric_second(metric, T)) <= 1e-13
+
+
+def test_invalid_mesh_reports_location():
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(3, (2, 2, 2), 1)
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), 3)
+    x2 = mesh.dof_vector().reshape(3, -1)
+    interior = np.nonzero(~mesh.fixed_mask.any(axis=0))[0]
+    x2[0, interior[0]] += 2.0
+    with pytest.raises(P.InvalidMeshError) as err:
+        p.objective(x2.ravel())
+    om = O.OracleProblem(O.box_mesh(3, (2, 2, 2), 1), 303, 3)
+    with pytest.raises(O.InvalidMesh) as oerr:
+        om.objective(x2.ravel())
+    assert (err.value.element, err.value.point) == (oerr.value.element, oerr.value.point)
+    assert err.value.value == pytest.approx(oerr.value.value, rel=1e-13)
+    with pytest.raises(P.InvalidMeshError):
+        p.hessian_setup(x2.ravel())
+    assert p.min_det_jacobian(x2.ravel()) < 0
+
+
+def test_properties_at_larger_size(rng):
+    """Size-independent checks at ~1e6 DOFs: symmetry, linearity, FD of gradient."""
+    import torch
+
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(3, (24, 24, 24), 2)
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), 4)
+    om = O.box_mesh(3, (24, 24, 24), 2)
+    x = torch.from_numpy(O.perturb(om, rng, 0.2)).cuda()
+    free = ~p.dmesh.fixed_mask
+    u = torch.randn(mesh.n_dofs, dtype=torch.float64, device="cuda") * free
+    v = torch.randn(mesh.n_dofs, dtype=torch.float64, device="cuda") * free
+    qd = p.hessian_setup(x)
+    Hu, Hv = p.hessian_apply(qd, u), p.hessian_apply(qd, v)
+    lhs, rhs = float(u @ Hv), float(v @ Hu)
+    assert abs(lhs - rhs) <= 1e-11 * max(1.0, abs(lhs))
+    H2 = p.hessian_apply(qd, 1.7 * u - 0.4 * v)
+    assert float((H2 - (1.7 * Hu - 0.4 * Hv)).norm() / H2.norm()) <= 1e-13
+    eps = 1e-5
+    fd = (p.gradient(x + eps * v) - p.gradient(x - eps * v)) / (2 * eps)
+    assert float((Hv - fd).norm() / fd.norm()) <= 1e-5
+
+
+def test_minres_matches_reference():
+    import torch
+
+    import paper_2205_12721_b200 as P
+    g = load_golden("minres_dense")
+    A = torch.from_numpy(g["A"]).cuda()
+    pre = P.jacobi_preconditioner(np.diag(g["A"]).copy())
+    r = P.minres(lambda v: A @ v, g["b"], P.MinresConfig(max_iterations=25, rel_tolerance=1e-10), pre)
+    assert r.iterations == int(g["iterations"])
+    assert rel(r.x, g["x"]) <= 1e-12
+    assert np.allclose(r.residual_history, g["history"], rtol=1e-10, atol=1e-14)
+
+
+def test_minres_edge_cases():
+    import torch
+
+    import paper_2205_12721_b200 as P
+    b = np.random.default_rng(1).standard_normal(8)
+    r = P.minres(lambda v: v, b, P.MinresConfig(max_iterations=10))
+    assert r.iterations == 1 and r.converged
+    assert np.allclose(r.x, b, atol=1e-14)
+    r0 = P.minres(lambda v: v, np.zeros(5), P.MinresConfig())
+    assert r0.iterations == 0 and np.array_equal(r0.x, np.zeros(5))
+    sign = torch.tensor([1.0, -1.0], dtype=torch.float64, device="cuda")
+    r2 = P.minres(lambda v: sign * v, np.array([1.0, 1.0]), P.MinresConfig(max_iterations=10, rel_tolerance=1e-13))
+    assert r2.iterations <= 2 and np.allclose(r2.x, [1.0, -1.0], atol=1e-12)
+    with pytest.raises(ValueError):
+        P.jacobi_preconditioner(np.array([np.nan, 1.0]))
+
+
+@pytest.mark.parametrize("name", golden_names("newton"))
+def test_newton_matches_reference_trace(name):
+    import paper_2205_12721_b200 as P
+    g = load_golden(name)
+    mesh = P.build_box(int(g["dim"]), tuple(int(c) for c in g["counts"]), int(g["order"]))
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId(int(g["metric"])),
+                                              P.TargetSpec(P.TargetKind.IDEAL_UNIT)), int(g["n_quad"]))
+    res = P.newton_solve(g["x0"], p, P.NewtonConfig(max_iterations=int(g["iters"])),
+                         P.MinresConfig(preconditioned=bool(g["precond"])))
+    want = g["records"]
+    assert res.trace.newton_iterations == len(want)
+    for rec, ref in zip(res.trace.records, want):
+        assert rec.alpha == ref[0]
+        assert rec.minres_iterations == int(ref[3])
+        assert rec.objective == pytest.approx(ref[1], rel=1e-9, abs=1e-13)
+        assert rec.grad_norm == pytest.approx(ref[2], rel=1e-8, abs=1e-13)
+    assert rel(res.x, g["x"]) <= 1e-10
+    assert p.objective(res.x) == pytest.approx(float(g["f_final"]), rel=1e-9, abs=1e-13)
+
+
+def test_unsupported_configuration_fails_loudly():
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(3, (2, 2, 2), 2)
+    with pytest.raises(P._lib.TmopLibraryError if hasattr(P, "_lib") else RuntimeError):
+        P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), 12)
