@@ -1,0 +1,359 @@
+"""Benchmark of the TMOP Hessian action (AddMultGradPA) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], "C3"): 3D hex perturbed unit cube,
+p = 2, 160^3 elements (99.2 M DOFs), n_q = p + 2 = 4, mu_303, ideal-shape
+target; x = uniform lattice + 0.2 * (h/p^2) * U(-1, 1) on free components
+(seed 20240901), v ~ N(0, 1) (seed 1).  One step = one Hessian action over
+the whole mesh; metric = N_dof / t_step (GDOF/s).  Inputs (46 GB of Q-data)
+are far larger than L2, so no flush is needed between steps.
+
+Also reported: per-order throughput (p = 1..4 at ~1e8 DOFs, p = 1 at 2.4e7),
+the roofline of the dominant kernel (element kernel, HBM-bound), e2e through
+the public API with pinned host buffers, one Newton iteration (paper
+protocol: MINRES fixed at 20) and the CPU baseline (C/OpenMP oracle port of
+the reference apply, bounded sample).  `--impl reference` times only the CPU
+port on the host cores (the reference itself is Python and cannot travel).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 20240901
+ORDERS = {1: (200, 3), 2: (160, 4), 3: (107, 5), 4: (80, 6)}   # p -> (elements per axis, n_q)
+HEADLINE_P = 2
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def perturbed_x(mesh, amplitude=0.2, seed=SEED):
+    """Reference test recipe (tests/oracles.py:121-131) restated for inputs."""
+    gap = (1.0 / max(mesh.element_counts)) / mesh.order ** 2
+    rng = np.random.default_rng(seed)
+    x = mesh.coords.ravel().copy()
+    j = amplitude * gap * rng.uniform(-1.0, 1.0, x.shape)
+    j[mesh.fixed_mask.ravel()] = 0.0
+    return x + j
+
+
+def apply_bytes(dim, order, nq, ne, n_dofs):
+    """SURVEY 8(d) yardstick per apply: reference Q-data + restriction + v + y."""
+    Q, n = nq ** dim, order + 1
+    return 8 * (4 + 2 * dim * dim) * ne * Q + 4 * ne * n ** dim + 16 * n_dofs
+
+
+def element_kernel_bytes(dim, order, nq, ne, n_dofs):
+    """Algorithmic bytes of one element-kernel launch: Q-data (22 fp64 / point)
+    + restriction (int32) + one read of v + the E-vector write."""
+    Q, n = nq ** dim, order + 1
+    return 8 * (4 + 2 * dim * dim) * ne * Q + 4 * ne * n ** dim + 8 * n_dofs + 8 * dim * ne * n ** dim
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out = self.proc.communicate(timeout=5)[0]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            f = [t.strip() for t in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[2:6]):
+                if val.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_problem(order, n, nq, device):
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(3, (n, n, n), order)
+    prob = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), nq,
+                         device=device)
+    return mesh, prob
+
+
+def time_applies(prob, qd, v, y, steps, warmup):
+    """Device-resident steps; per-phase CUDA events on the launching stream."""
+    import torch
+    lib, ctx = prob.lib, prob.ctx
+    from paper_2205_12721_b200 import _lib
+    s = torch.cuda.current_stream()
+    prob._sync_stream()
+    for _ in range(warmup):
+        prob.hessian_apply(qd, v, out=y)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    torch.cuda.synchronize()
+    for k in range(steps):
+        ev[k][0].record(s)
+        _lib.check(lib.tmop_hessian_apply_elements(ctx, _lib.ptr(qd.data), _lib.ptr(v)), "elements")
+        ev[k][1].record(s)
+        _lib.check(lib.tmop_hessian_apply_gather(ctx, _lib.ptr(v), _lib.ptr(y)), "gather")
+        ev[k][2].record(s)
+    torch.cuda.synchronize()
+    total = ev[0][0].elapsed_time(ev[-1][2]) / 1e3
+    elem = [e[0].elapsed_time(e[1]) / 1e3 for e in ev]
+    gath = [e[1].elapsed_time(e[2]) / 1e3 for e in ev]
+    return total, statistics.mean(elem), statistics.mean(gath)
+
+
+def run_order(order, n, nq, steps, warmup, device, with_e2e=False, with_newton=False, sampler_index=None):
+    import torch
+    t0 = time.time()
+    mesh, prob = build_problem(order, n, nq, device)
+    x = torch.from_numpy(perturbed_x(mesh)).to(device)
+    rng = np.random.default_rng(1)
+    v = torch.from_numpy(rng.standard_normal(mesh.n_dofs)).to(device)
+    y = torch.empty_like(v)
+    qd = prob.hessian_setup(x)
+    setup_s = time.time() - t0
+    res = {"order": order, "elements": mesh.n_elements, "n_quad": nq, "n_dofs": mesh.n_dofs,
+           "qdata_gb": qd.nbytes / 1e9}
+    clocks = None
+    if sampler_index is not None:
+        with ClockSampler(sampler_index) as cs:
+            total, t_elem, t_gath = time_applies(prob, qd, v, y, steps, warmup)
+        clocks = cs.summary()
+    else:
+        total, t_elem, t_gath = time_applies(prob, qd, v, y, steps, warmup)
+    res.update(ms_per_step=1e3 * total / steps, gdofs=mesh.n_dofs * steps / total / 1e9,
+               t_elem_ms=1e3 * t_elem, t_gather_ms=1e3 * t_gath,
+               elem_bytes=element_kernel_bytes(3, order, nq, mesh.n_elements, mesh.n_dofs),
+               apply_bytes=apply_bytes(3, order, nq, mesh.n_elements, mesh.n_dofs),
+               host_setup_s=setup_s)
+    if with_e2e:
+        # public API with pinned host buffers: H2D of v + apply + D2H of y every step
+        vh = v.cpu().pin_memory()
+        for _ in range(max(1, warmup)):
+            prob.hessian_apply(qd, vh)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(steps):
+            yh = prob.hessian_apply(qd, vh)
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - t) / steps
+        res["e2e"] = {"value": mesh.n_dofs / te / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * mesh.n_dofs,
+                      "d2h_bytes_per_step": 8 * yh.numel(), "ms_per_step": 1e3 * te}
+        ref = y.cpu()
+        res["e2e_matches_device"] = bool(torch.equal(yh, ref))
+    if with_newton:
+        res["newton"] = newton_iteration(prob, x)
+    del qd
+    torch.cuda.synchronize()
+    return res, clocks
+
+
+def newton_iteration(prob, x):
+    """One Newton iteration, paper protocol (MINRES fixed at 20 iterations,
+    PAPER.md:1002-1004): setup + diagonal + MINRES + line search."""
+    import torch
+
+    import paper_2205_12721_b200 as P
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    g = prob.gradient(x)
+    f = prob.objective(x)
+    ng = float(torch.linalg.norm(g))
+    torch.cuda.synchronize()
+    t_pre = time.perf_counter() - t
+    t = time.perf_counter()
+    qd = prob.hessian_setup(x)
+    pre = P.jacobi_preconditioner(prob.hessian_diagonal(qd), prob.ctx)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t
+    t = time.perf_counter()
+    mr = P.minres(lambda vv: prob.hessian_apply(qd, vv), g,
+                  P.MinresConfig(max_iterations=20, rel_tolerance=1e-300), pre, prob.ctx)
+    torch.cuda.synchronize()
+    t_minres = time.perf_counter() - t
+    t = time.perf_counter()
+    ls = P.line_search(x, mr.x, prob, f, ng, ctx=prob.ctx)
+    torch.cuda.synchronize()
+    t_ls = time.perf_counter() - t
+    return {"ms": 1e3 * (t_setup + t_minres + t_ls), "setup_diag_ms": 1e3 * t_setup,
+            "minres_ms": 1e3 * t_minres, "minres_iterations": mr.iterations, "line_search_ms": 1e3 * t_ls,
+            "alpha": ls.alpha, "initial_gradient_ms": 1e3 * t_pre}
+
+
+def cpu_baseline(order=2, n=40, budget_s=12.0):
+    """C/OpenMP oracle port of the reference apply on a bounded sample."""
+    from oracle import tmop_oracle as O
+    from oracle.cpu_apply import CpuApply
+    nq = order + 2
+    om = O.box_mesh(3, (n, n, n), order)
+    prob = O.OracleProblem(om, O.MU_303, nq)
+    x = O.perturb(om, np.random.default_rng(SEED), 0.2)
+    v = np.random.default_rng(1).standard_normal(x.shape)
+    qd = prob.hessian_setup(x)
+    ca = CpuApply(prob, qd)
+    ca(v)
+    times = []
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < budget_s or len(times) < 3:
+        t = time.perf_counter()
+        ca(v)
+        times.append(time.perf_counter() - t)
+    best = min(times)
+    return {"value": om.n_dofs / best / 1e9, "unit": "GDOF/s", "cores": ca.threads, "kind": "port",
+            "sample": f"p={order} {n}^3 elements ({om.n_dofs} DOFs), n_q={nq}, mu_303; best of {len(times)} "
+                      f"applies of the C/OpenMP oracle port (oracle/tmop_cpu.c)",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--orders", default="1,2,3,4", help="orders reported under per_order")
+    ap.add_argument("--no-newton", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    n_h, nq_h = ORDERS[HEADLINE_P]
+    config = {"workload": f"C3: 3D hex perturbed unit cube, p={HEADLINE_P}, {n_h}^3 elements, n_q={nq_h}, "
+                          f"mu_303, ideal-shape target (amp 0.2 h/p^2, seed {SEED})",
+              "order": HEADLINE_P, "elements_per_axis": n_h, "n_quad": nq_h, "metric_id": 303,
+              "l2": "inputs > L2 (Q-data >> 126 MB), no flush", "parallelism": f"replicas x{world}"}
+    metric = "3D TMOP Hessian-action GDOF/s (p=2, ~1e8 DOFs)"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cb = cpu_baseline(HEADLINE_P, 40, budget_s=max(3.0, 1.5 * args.steps))
+        line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": "GDOF/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+                "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "GDOF/s", "h2d_bytes_per_step": 0,
+                                            "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    device = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
+    torch.cuda.set_device(device)
+    if world > 1:
+        torch.distributed.barrier()
+    head, clocks = run_order(HEADLINE_P, n_h, nq_h, args.steps, args.warmup, device, with_e2e=True,
+                             with_newton=not args.no_newton, sampler_index=local)
+    # whole-job aggregate: max time over ranks (replicas, weak scaling)
+    ms = torch.tensor([head["ms_per_step"]], dtype=torch.float64, device=device)
+    if world > 1:
+        torch.distributed.all_reduce(ms, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(ms.item())
+    value = world * head["n_dofs"] / (ms_max / 1e3) / 1e9
+    per_order = {}
+    for p in [int(s) for s in args.orders.split(",") if s.strip()]:
+        if p == HEADLINE_P:
+            per_order[str(p)] = {k: head[k] for k in ("gdofs", "ms_per_step", "n_dofs", "elements", "n_quad",
+                                                      "t_elem_ms", "t_gather_ms")}
+            continue
+        n, nq = ORDERS[p]
+        r, _ = run_order(p, n, nq, max(3, args.steps // 2), args.warmup, device)
+        r["roofline_frac_elem"] = r["elem_bytes"] / (r["t_elem_ms"] / 1e3) / 1e9 / peaks()[0]
+        per_order[str(p)] = {k: r[k] for k in ("gdofs", "ms_per_step", "n_dofs", "elements", "n_quad",
+                                               "t_elem_ms", "t_gather_ms", "roofline_frac_elem")}
+    if rank != 0:
+        torch.distributed.barrier()
+        return
+    peak, peak_src = peaks()
+    achieved = head["elem_bytes"] / (head["t_elem_ms"] / 1e3) / 1e9
+    line = {
+        "metric": metric, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (perturbed cube, seeded)", "config": config,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "elem_kernel<3,3,4,K_APPLY>",
+                     "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
+                     "algorithmic_bytes_per_launch": head["elem_bytes"],
+                     "kernel_share_of_step": head["t_elem_ms"] / head["ms_per_step"]},
+        "apply_roofline": {"yardstick_bytes": head["apply_bytes"],
+                           "achieved_gbs": head["apply_bytes"] / (head["ms_per_step"] / 1e3) / 1e9,
+                           "frac": head["apply_bytes"] / (head["ms_per_step"] / 1e3) / 1e9 / peak},
+        "e2e": head["e2e"], "e2e_matches_device": head.get("e2e_matches_device"),
+        "gpu_launches": 2 * args.steps, "clocks": clocks, "per_order": per_order,
+        "qdata_gb": head["qdata_gb"],
+    }
+    if "newton" in head:
+        line["newton_iteration"] = head["newton"]
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(HEADLINE_P, 40)
+    print(json.dumps(line))
+    if world > 1:
+        torch.distributed.barrier()
+
+
+if __name__ == "__main__":
+    main()

@@ -94,6 +94,13 @@ int tmop_hessian_setup(tmop_ctx *ctx, const double *x, double *qdata,
  * dofs, y = v on constrained dofs. */
 int tmop_hessian_apply(tmop_ctx *ctx, const double *qdata, const double *v,
                        double *y);
+/* The two phases of tmop_hessian_apply, exposed for per-kernel timing and
+ * for fusing the E->L sum with solver updates: the element kernel (writes
+ * the context's element-blocked E-vector) and the deterministic E->L sum
+ * with the constrained-dof fix-up. */
+int tmop_hessian_apply_elements(tmop_ctx *ctx, const double *qdata,
+                                const double *v);
+int tmop_hessian_apply_gather(tmop_ctx *ctx, const double *v, double *y);
 /* AssembleGradDiagonalPA: hessian_diagonal (operator.py:420-459). */
 int tmop_hessian_diagonal(tmop_ctx *ctx, const double *qdata, double *diag);
 /* AddMultPA: gradient (operator.py:328-346). */

@@ -49,6 +49,8 @@ _SIGS = {
     "tmop_ctx_set_limiting": [_P, _P, _P, _D, _D],
     "tmop_hessian_setup": [_P, _P, _P, _P],
     "tmop_hessian_apply": [_P, _P, _P, _P],
+    "tmop_hessian_apply_elements": [_P, _P, _P],
+    "tmop_hessian_apply_gather": [_P, _P, _P],
     "tmop_hessian_diagonal": [_P, _P, _P],
     "tmop_gradient": [_P, _P, _P, _P],
     "tmop_objective": [_P, _P, _P, _P],

@@ -236,6 +236,21 @@ int tmop_hessian_apply(tmop_ctx *c, const double *qdata, const double *v, double
   return TMOP_OK;
 }
 
+int tmop_hessian_apply_elements(tmop_ctx *c, const double *qdata, const double *v) {
+  if (!c || !qdata || !v) return fail(TMOP_ERR_ARG, "NULL argument");
+  ElemArgs a = base_args(c);
+  a.in = v;
+  a.qdata = qdata;
+  return run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
+}
+
+int tmop_hessian_apply_gather(tmop_ctx *c, const double *v, double *y) {
+  if (!c || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
+  launch_e2l(c->dim, c->nn, c->NP, c->l2e_off, c->l2e_idx, c->E, c->fixed, 0, v, nullptr, y, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
 int tmop_hessian_diagonal(tmop_ctx *c, const double *qdata, double *diag) {
   if (!c || !qdata || !diag) return fail(TMOP_ERR_ARG, "NULL argument");
   ElemArgs a = base_args(c);

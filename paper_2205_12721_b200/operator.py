@@ -245,24 +245,34 @@ class TmopProblem:
             self._stream = s
 
     def _in(self, x):
-        """(device float64 contiguous tensor, came_from_numpy)."""
+        """(device float64 contiguous tensor, origin) with origin False for a
+        device tensor, "numpy" for numpy input and "torch" for a host torch
+        tensor (pinned host tensors are copied asynchronously)."""
         torch = _torch()
         if _is_torch(x):
             t = x.detach()
+            origin = False if t.is_cuda else "torch"
             if t.device != self.device or t.dtype != torch.float64:
-                t = t.to(device=self.device, dtype=torch.float64)
+                t = t.to(device=self.device, dtype=torch.float64, non_blocking=True)
             t = t.reshape(-1).contiguous()
-            host = False
         else:
             t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64).reshape(-1)).to(self.device)
-            host = True
+            origin = "numpy"
         if t.numel() != self.mesh.n_dofs:
             raise ValueError(f"expected a T-vector of length {self.mesh.n_dofs}, got {t.numel()}")
         self._sync_stream()
-        return t, host
+        return t, origin
 
-    def _out(self, t, host):
-        return t.cpu().numpy() if host else t
+    def _out(self, t, origin):
+        if not origin:
+            return t
+        if origin == "numpy":
+            return t.cpu().numpy()
+        torch = _torch()
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return h
 
     def _det(self):
         st = self._status.cpu().numpy()
