@@ -263,16 +263,27 @@ class TmopProblem:
         self._sync_stream()
         return t, origin
 
-    def _out(self, t, origin):
+    def _out(self, t, origin, out=None):
+        """Return the device result `t` in the caller's currency.  A host torch
+        `out` (ideally pinned) receives an asynchronous D2H copy."""
+        torch = _torch()
+        if out is not None and not out.is_cuda:
+            out.view(-1).copy_(t, non_blocking=True)
+            torch.cuda.current_stream(self.device).synchronize()
+            return out
         if not origin:
             return t
         if origin == "numpy":
             return t.cpu().numpy()
-        torch = _torch()
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         h.copy_(t, non_blocking=True)
         torch.cuda.current_stream(self.device).synchronize()
         return h
+
+    @staticmethod
+    def _dev_out(out, like):
+        torch = _torch()
+        return out if (out is not None and out.is_cuda) else torch.empty_like(like)
 
     def _det(self):
         st = self._status.cpu().numpy()
@@ -336,13 +347,13 @@ class TmopProblem:
     def gradient(self, x, out=None):
         torch = _torch()
         xt, host = self._in(x)
-        g = torch.empty_like(xt) if out is None else out
+        g = self._dev_out(out, xt)
         _lib.check(self.lib.tmop_gradient(self._ctx, _lib.ptr(xt), _lib.ptr(g), _lib.ptr(self._status)),
                    "tmop_gradient")
         self._count("gradient")
         md, _ = self._det()
         self._raise_if_inverted(xt, md)
-        return self._out(g, host)
+        return self._out(g, host, out)
 
     def hessian_setup(self, x) -> HessQData:
         torch = _torch()
@@ -363,11 +374,11 @@ class TmopProblem:
         (operator.py:401-418)."""
         torch = _torch()
         vt, host = self._in(v)
-        y = torch.empty_like(vt) if out is None else out
+        y = self._dev_out(out, vt)
         _lib.check(self.lib.tmop_hessian_apply(self._ctx, _lib.ptr(qdata.data), _lib.ptr(vt), _lib.ptr(y)),
                    "tmop_hessian_apply")
         self._count("apply")
-        return self._out(y, host)
+        return self._out(y, host, out)
 
     def hessian_diagonal(self, qdata: HessQData, out=None):
         torch = _torch()

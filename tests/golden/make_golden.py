@@ -100,6 +100,22 @@ def minres_case(name, n=40, seed=7):
                         iterations=r.iterations, history=np.array(r.residual_history))
 
 
+def minres_conditioned_case(name, n=200, seed=11, indefinite=True):
+    """Well-conditioned system: few iterations, rounding does not amplify."""
+    rng = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = rng.uniform(1.0, 4.0, n)
+    if indefinite:
+        lam[: n // 3] *= -1.0
+    A = (q * lam) @ q.T
+    A = 0.5 * (A + A.T)
+    b = rng.standard_normal(n)
+    pre = tb.jacobi_preconditioner(np.diag(A).copy())
+    r = tb.minres(lambda v: A @ v, b, tb.MinresConfig(max_iterations=12, rel_tolerance=1e-10), pre)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), A=A, b=b, x=r.x,
+                        iterations=r.iterations, history=np.array(r.residual_history))
+
+
 def metric_points(name):
     rng = np.random.default_rng(SEED)
     out = {}
@@ -145,6 +161,7 @@ def main():
     newton_case("newton_3d_p1_4c_mu303_noprec", 3, (4, 4, 4), 1, 3, 303, iters=2,
                 precond=False)
     minres_case("minres_dense")
+    minres_conditioned_case("minres_wellcond")
     metric_points("metric_points")
     kershaw_case("kershaw_6x2x2_p2")
     print("golden fixtures written to", HERE)

@@ -170,17 +170,23 @@ def test_properties_at_larger_size(rng):
     assert float((Hv - fd).norm() / fd.norm()) <= 1e-5
 
 
-def test_minres_matches_reference():
+@pytest.mark.parametrize("name,xtol,its", [("minres_wellcond", 1e-12, 12), ("minres_dense", 1e-3, 25)])
+def test_minres_matches_reference(name, xtol, its):
+    """minres_wellcond: 12 iterations on a conditioned indefinite system, where
+    rounding does not amplify (a 1e-16 perturbation of A moves x by 2e-13).
+    minres_dense: 25 iterations on a 40x40 random indefinite system where the
+    Lanczos vectors lose orthogonality; a 1e-16 perturbation of A already moves
+    x by 2e-5 in the oracle, so only 1e-3 agreement is meaningful there."""
     import torch
 
     import paper_2205_12721_b200 as P
-    g = load_golden("minres_dense")
+    g = load_golden(name)
     A = torch.from_numpy(g["A"]).cuda()
     pre = P.jacobi_preconditioner(np.diag(g["A"]).copy())
-    r = P.minres(lambda v: A @ v, g["b"], P.MinresConfig(max_iterations=25, rel_tolerance=1e-10), pre)
+    r = P.minres(lambda v: A @ v, g["b"], P.MinresConfig(max_iterations=its, rel_tolerance=1e-10), pre)
     assert r.iterations == int(g["iterations"])
-    assert rel(r.x, g["x"]) <= 1e-12
-    assert np.allclose(r.residual_history, g["history"], rtol=1e-10, atol=1e-14)
+    assert rel(r.x, g["x"]) <= xtol
+    assert np.allclose(r.residual_history, g["history"], rtol=max(xtol, 1e-10), atol=1e-14)
 
 
 def test_minres_edge_cases():
