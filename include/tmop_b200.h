@@ -14,12 +14,14 @@
  * (n_elements, (order+1)^dim) with the local x index fastest.
  *
  * Q-data (the partially assembled Hessian, reference HessQData
- * operator.py:91-138) is stored ELEMENT-BLOCKED: qdata[e][field][q],
- * fields = tmop_qdata_fields(ctx) doubles per quadrature point.  For the
- * template metrics (mu_2, mu_7, mu_55, mu_303) the fields are
- * c_id, c_ts, c_ss, c_x (scaled by w_q * coef), S (d*d), T (d*d) -- the
- * reference's 4 + 2 d^2 values per point, in the reference order.  For
- * mu_302 / mu_321 (no reference equivalent) the fields are w (1), S, T.
+ * operator.py:91-138) is stored ELEMENT-BLOCKED and LEAN:
+ * qdata[e * stride + field * Q + q], stride = tmop_qdata_stride(ctx) (even,
+ * so each element block is 16-byte aligned for TMA bulk copies), fields =
+ * T (d*d), k0, itau = 1/det T -- d^2 + 2 doubles per point instead of the
+ * reference's 4 + 2 d^2.  S = T^{-T} and the four Hessian-template
+ * coefficients are recomputed from them;
+ * tmop_qdata_to_reference() materialises the reference's planar
+ * coeffs / s_mat / t_mat arrays for inspection and parity tests.
  */
 #ifndef TMOP_B200_H
 #define TMOP_B200_H
@@ -75,8 +77,14 @@ int tmop_ctx_destroy(tmop_ctx *ctx);
 int tmop_ctx_set_stream(tmop_ctx *ctx, void *stream);
 /* Change target scale (build_targets, metrics.py:333-345) after creation. */
 int tmop_ctx_set_target(tmop_ctx *ctx, double inv_scale, double det_w);
-int tmop_qdata_fields(const tmop_ctx *ctx);            /* doubles per point */
-int64_t tmop_qdata_size(const tmop_ctx *ctx);          /* doubles total     */
+int tmop_qdata_fields(const tmop_ctx *ctx);            /* doubles per point   */
+int64_t tmop_qdata_stride(const tmop_ctx *ctx);        /* doubles per element */
+int64_t tmop_qdata_size(const tmop_ctx *ctx);          /* doubles total       */
+/* Reference-layout view of the Q-data: (fields_ref, n_elements * Q) planar,
+ * fields_ref = 4 + 2 d^2 (c_id, c_ts, c_ss, c_x, S, T) for template metrics
+ * and 1 + 2 d^2 (w, S, T) for mu_302 / mu_321 (operator.py:105-113). */
+int tmop_qdata_reference_fields(const tmop_ctx *ctx);
+int tmop_qdata_to_reference(tmop_ctx *ctx, const double *qdata, double *out);
 /* Configure the displacement-limiting term (operator.py:57-76, 463-533):
  * x0 (reference positions, T-vector) and delta_nodal (n_nodes, or NULL for
  * the scalar delta) are DEVICE pointers; weight > 0 enables, 0 disables. */

@@ -45,7 +45,10 @@ _SIGS = {
     "tmop_ctx_set_stream": [_P, _P],
     "tmop_ctx_set_target": [_P, _D, _D],
     "tmop_qdata_fields": [_P],
+    "tmop_qdata_stride": [_P],
     "tmop_qdata_size": [_P],
+    "tmop_qdata_reference_fields": [_P],
+    "tmop_qdata_to_reference": [_P, _P, _P],
     "tmop_ctx_set_limiting": [_P, _P, _P, _D, _D],
     "tmop_hessian_setup": [_P, _P, _P, _P],
     "tmop_hessian_apply": [_P, _P, _P, _P],
@@ -66,7 +69,7 @@ _SIGS = {
     "tmop_minres_step": [_P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _D, _P, _INT],
     "tmop_last_error": [],
 }
-_RESTYPES = {"tmop_qdata_size": _I64, "tmop_last_error": C.c_char_p}
+_RESTYPES = {"tmop_qdata_size": _I64, "tmop_qdata_stride": _I64, "tmop_last_error": C.c_char_p}
 
 EXPORTED = tuple(_SIGS)
 

@@ -198,12 +198,37 @@ int tmop_ctx_set_target(tmop_ctx *c, double inv_scale, double det_w) {
 
 int tmop_qdata_fields(const tmop_ctx *c) {
   if (!c) return -1;
-  return metric_is_template(c->metric) ? 4 + 2 * c->dim * c->dim : 1 + 2 * c->dim * c->dim;
+  return c->dim * c->dim + 2;
+}
+
+int64_t tmop_qdata_stride(const tmop_ctx *c) {
+  if (!c) return -1;
+  return ((int64_t)tmop_qdata_fields(c) * c->QP + 1) & ~(int64_t)1;
 }
 
 int64_t tmop_qdata_size(const tmop_ctx *c) {
   if (!c) return -1;
-  return (int64_t)tmop_qdata_fields(c) * c->QP * c->ne;
+  return tmop_qdata_stride(c) * c->ne;
+}
+
+int tmop_qdata_reference_fields(const tmop_ctx *c) {
+  if (!c) return -1;
+  return (metric_is_template(c->metric) ? 4 : 1) + 2 * c->dim * c->dim;
+}
+
+int tmop_qdata_to_reference(tmop_ctx *c, const double *qdata, double *out) {
+  if (!c || !qdata || !out) return fail(TMOP_ERR_ARG, "NULL argument");
+  const int64_t nq = c->ne * c->QP;
+  if (nq == 0) return TMOP_OK;
+  const int nt = 128;
+  const unsigned grid = (unsigned)((nq + nt - 1) / nt);
+  const int qs = (int)tmop_qdata_stride(c);
+  if (c->dim == 2)
+    qdata_expand_kernel<2><<<grid, nt, 0, c->stream>>>(c->metric, c->ne, c->QP, qs, qdata, out);
+  else
+    qdata_expand_kernel<3><<<grid, nt, 0, c->stream>>>(c->metric, c->ne, c->QP, qs, qdata, out);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
 }
 
 int tmop_ctx_set_limiting(tmop_ctx *c, const double *, const double *, double, double) {

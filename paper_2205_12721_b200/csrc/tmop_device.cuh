@@ -168,6 +168,41 @@ __device__ __forceinline__ void metric_second_coeffs(int metric, double tau, dou
   }
 }
 
+// ---- lean Q-data (the B200 format) -------------------
+// Per point: T (d*d), k0, itau = 1/det T.  S = cof(T) * itau and I1 = |T|^2
+// are recomputed in the apply, and the four template coefficients follow
+// from (k0, itau, I1) -- 11 doubles per 3D point instead of the reference's
+// 4 + 2 d^2 = 22 (operator.py:91-113), with identical information.
+//   mu_303: k0 = sw r, r = tau^{-2/3}:  c = k0 (2/3, -4/9, 4/27 I1, 2/9 I1)
+//   mu_2:   k0 = sw / tau:              c = k0 (1, -1, I1/2, I1/2)
+//   mu_7:   k0 = sw:                    c = k0 (2(1+it2), -4 it2, 4 I1 it2, 2 I1 it2)
+//   mu_55:  k0 = sw:                    c = k0 (0, 0, 2 tau(2 tau-1), -2 tau(tau-1))
+//   mu_302 / mu_321: k0 = sw (non-template action, nt_hess)
+__device__ __forceinline__ double lean_k0(int metric, double sw, double tau) {
+  switch (metric) {
+    case MU303: return sw * (1.0 / cbrt(tau * tau));
+    case MU2: return sw / tau;
+    default: return sw;
+  }
+}
+__device__ __forceinline__ void lean_coeffs(int metric, double k0, double itau, double I1, double (&c)[4]) {
+  switch (metric) {
+    case MU303: {
+      const double h = k0 * I1;
+      c[0] = (2.0 / 3.0) * k0; c[1] = -(4.0 / 9.0) * k0; c[2] = (4.0 / 27.0) * h; c[3] = (2.0 / 9.0) * h;
+    } break;
+    case MU2: { const double h = 0.5 * k0 * I1; c[0] = k0; c[1] = -k0; c[2] = h; c[3] = h; } break;
+    case MU7: {
+      const double it2 = itau * itau, h = k0 * it2;
+      c[0] = 2.0 * k0 * (1.0 + it2); c[1] = -4.0 * h; c[2] = 4.0 * h * I1; c[3] = 2.0 * h * I1;
+    } break;
+    default: /* MU55 */ {
+      const double tau = 1.0 / itau;
+      c[0] = 0.0; c[1] = 0.0; c[2] = 2.0 * k0 * tau * (2.0 * tau - 1.0); c[3] = -2.0 * k0 * tau * (tau - 1.0);
+    }
+  }
+}
+
 // z = H g for the template block  c0 I + c1 (S(x)T + T(x)S) + c2 S(x)S + c3 S_mp S_on
 // (_kernels.py:235-258).
 template <int D>
@@ -271,6 +306,40 @@ __device__ __forceinline__ void nt_hess(int metric, double w, const double (&S)[
 #pragma unroll
       for (int j = 0; j < D; ++j) z[i][j] = w * (2.0 * g[i][j] - 2.0 * dM[i][j]);
   }
+}
+
+// ------------------------------------------- TMA bulk copy + mbarrier
+// One elected thread streams a contiguous global range into shared memory
+// with cp.async.bulk (the TMA engine, no register staging); consumers wait
+// on an mbarrier phase.  Sizes and addresses must be multiples of 16 B.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
 }
 
 // ------------------------------------------------ deterministic reductions

@@ -56,8 +56,15 @@ struct Cfg {
   static constexpr int R1 = DIM == 3 ? cmax(cmax(3 * NP, 9 * Q * Q * N), QP) : cmax(cmax(2 * NP, 4 * QP), 2 * Q * N);
   static constexpr int R2 = DIM == 3 ? cmax(6 * Q * N * N, 9 * QP) : cmax(4 * Q * N, 2 * QP);
   static constexpr int PER = R1 + R2;
-  static constexpr int EPB = cclamp(8192 / PER, 1, 32);  // ~64 KB of shared memory per CTA
-  static constexpr int SMEM = EPB * PER * 8;
+  // lean Q-data: T (d*d), k0, itau per point; element stride rounded to an
+  // even number of doubles so every element block is 16-byte aligned (TMA).
+  static constexpr int F = DIM * DIM + 2;
+  static constexpr int QS = (F * QP + 1) & ~1;
+  // elements per CTA: work arrays + staged Q-data in ~112 KB (2 CTAs / SM)
+  static constexpr int EPB = cclamp(14336 / (PER + QS), 1, 32);
+  static constexpr int QOFF = (EPB * PER + 1) & ~1;          // Q-data staging offset (doubles)
+  static constexpr int SMEM = EPB * PER * 8;                 // kernels without staging
+  static constexpr int SMEM_TMA = (QOFF + EPB * QS) * 8;     // Hessian-action kernels
 };
 
 struct ElemArgs {
@@ -65,8 +72,8 @@ struct ElemArgs {
   const int32_t *__restrict__ restr;
   const uint8_t *__restrict__ fixed;
   const double *__restrict__ in;      // x (positions) or v (direction), T-vector
-  const double *__restrict__ qdata;   // K_APPLY / K_DIAG input
-  double *__restrict__ qout;          // K_SETUP output
+  const double *__restrict__ qdata;   // K_APPLY / K_DIAG input (lean, element stride QS)
+  double *__restrict__ qout;          // K_SETUP output (lean)
   double *__restrict__ E;             // K_APPLY / K_GRAD / K_DIAG E-vector output
   double *__restrict__ part_sum;      // per-CTA partial sums (energy / volume)
   double *__restrict__ part_min;      // per-CTA partial min det
@@ -298,8 +305,7 @@ __device__ __forceinline__ void f1_2d(const Tab &t, const double *R1, double *R2
   }
 }
 
-// U (R2) -> grad[c*2+dir][qy][qx] (R1 is free; we write to R2 after a copy?)
-// To keep the ping-pong simple in 2D: U lives in R2, grad is written to R1.
+// U (R2) -> grad[c*2+dir][qy][qx] (R1)
 template <int N, int Q, int C>
 __device__ __forceinline__ void f2_2d(const Tab &t, const double *R2, double *G) {
   using CF = Cfg<2, N, Q>;
@@ -392,34 +398,81 @@ __device__ __forceinline__ void store_point(double *g, int stride, const double 
     for (int d = 0; d < D; ++d) g[(c * D + d) * stride] = A[c][d];
 }
 
+// Lean point record -> (T, S, coefficient scalars).  qd points at field 0 of
+// the point (field stride QP).
 template <int D>
-__host__ __device__ constexpr int qfields_template() { return 4 + 2 * D * D; }
-template <int D>
-__host__ __device__ constexpr int qfields_nt() { return 1 + 2 * D * D; }
+__device__ __forceinline__ void lean_load(const double *qd, int QP, double (&T)[D][D], double (&S)[D][D],
+                                          double &k0, double &itau) {
+  load_point<D>(qd, QP, T);
+  k0 = qd[D * D * QP];
+  itau = qd[(D * D + 1) * QP];
+  double C[D][D];
+  mcof<D>(T, C);
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) S[i][j] = C[i][j] * itau;
+}
+
+// z = (d2 mu / dT2 scaled) : g from a lean point record.
+template <int D, bool NTM>
+__device__ __forceinline__ void lean_hess(int metric, const double *qd, int QP, const double (&g)[D][D],
+                                          double (&z)[D][D]) {
+  double T[D][D], S[D][D], k0, itau;
+  lean_load<D>(qd, QP, T, S, k0, itau);
+  if constexpr (!NTM) {
+    double c[4];
+    lean_coeffs(metric, k0, itau, mfro2<D>(T), c);
+    hess_template<D>(c, S, T, g, z);
+  } else {
+    nt_hess<D>(metric, k0, S, T, g, z);
+  }
+}
 
 // ------------------------------------------------------ the kernel
 template <int DIM, int N, int Q, int KIND>
 __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
   using CF = Cfg<DIM, N, Q>;
-  constexpr int QP = CF::QP, EPB = CF::EPB;
-  extern __shared__ double smem[];
+  constexpr int QP = CF::QP, EPB = CF::EPB, QS = CF::QS;
+  constexpr bool APPLY = (KIND == K_APPLY || KIND == K_APPLY_NT);
+  extern __shared__ __align__(16) double smem[];
   double *R1 = smem;
   double *R2 = smem + EPB * CF::R1;
+  double *QB = smem + CF::QOFF;   // staged Q-data of the current group (apply only)
   __shared__ double red_v[ELEM_NT / 32];
   __shared__ int64_t red_i[ELEM_NT / 32];
+  __shared__ __align__(8) uint64_t qbar;
 
-  // The Hessian-action kernels are specialised per metric family so the
-  // template path does not carry the register footprint of the mu_302/321 one.
-  const bool tmpl = (KIND == K_APPLY) ? true : (KIND == K_APPLY_NT ? false : metric_is_template(a.metric));
   double acc = 0.0;
   MinLoc mn{DBL_MAX, LLONG_MAX};
 
+  // The Hessian action streams each group's Q-data (one contiguous block of
+  // EPB * QS doubles) into shared memory with one TMA bulk copy, issued a
+  // whole group ahead: the copy for group g + grid overlaps the transposed
+  // sweeps of group g and the gather / forward sweeps of the next group.
+  auto issue = [&](int64_t grp) {
+    const int64_t e0 = grp * EPB;
+    const int64_t cnt = (a.ne - e0) < EPB ? (a.ne - e0) : EPB;
+    const uint32_t bytes = (uint32_t)(cnt * QS * 8);
+    mbar_expect_tx(&qbar, bytes);
+    tma_load_1d(QB, a.qdata + e0 * QS, bytes, &qbar);
+  };
+  uint32_t phase = 0;
+  if constexpr (APPLY) {
+    if (threadIdx.x == 0) {
+      mbar_init(&qbar, 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (int64_t)blockIdx.x < a.ngroups) issue(blockIdx.x);
+  }
+
   for (int64_t grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
     const int64_t e0 = grp * EPB;
-    gather<DIM, N, Q, DIM, KIND == K_APPLY || KIND == K_APPLY_NT>(a, e0, R1);
+    gather<DIM, N, Q, DIM, APPLY>(a, e0, R1);
     __syncthreads();
     // ---- forward: gradients of the gathered field at the points
-    double *Gp;  // grad[c*DIM+dir][q] per element, stride R?
+    double *Gp;
     int gstride;
     if constexpr (DIM == 3) {
       f1_3d<N, Q, 3>(t, R1, R2);
@@ -436,6 +489,7 @@ __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const _
       Gp = R1;
       gstride = CF::R1;
     }
+    if constexpr (APPLY) mbar_wait(&qbar, phase);
     __syncthreads();
 
     // ---- point stage
@@ -447,26 +501,9 @@ __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const _
       double A[DIM][DIM];
       load_point<DIM>(gp, QP, A);
 
-      if constexpr (KIND == K_APPLY || KIND == K_APPLY_NT) {
+      if constexpr (APPLY) {
         double z[DIM][DIM];
-        if constexpr (KIND == K_APPLY) {
-          constexpr int F = qfields_template<DIM>();
-          const double *qd = a.qdata + eg * F * QP + q;
-          double c[4], S[DIM][DIM], T[DIM][DIM];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) c[k] = __ldg(qd + k * QP);
-          load_point<DIM>(qd + 4 * QP, QP, S);
-          load_point<DIM>(qd + (4 + DIM * DIM) * QP, QP, T);
-          hess_template<DIM>(c, S, T, A, z);
-        } else {
-          constexpr int F = qfields_nt<DIM>();
-          const double *qd = a.qdata + eg * F * QP + q;
-          double S[DIM][DIM], T[DIM][DIM];
-          const double wv = __ldg(qd);
-          load_point<DIM>(qd + QP, QP, S);
-          load_point<DIM>(qd + (1 + DIM * DIM) * QP, QP, T);
-          nt_hess<DIM>(a.metric, wv, S, T, A, z);
-        }
+        lean_hess<DIM, KIND == K_APPLY_NT>(a.metric, QB + e * QS + q, QP, A, z);
         store_point<DIM>(gp, QP, z);
       } else {
         // A is the Jacobian dx/dxi at the point
@@ -474,7 +511,7 @@ __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const _
         if constexpr (KIND == K_VOLUME) {
           acc += dj * wq<DIM, Q>(t, q);
         } else if constexpr (KIND == K_ELEMDET) {
-          R1[e * CF::R1 + q] = dj;  // (2D: grad lives in R1 too, but per-point in place is safe)
+          R1[e * CF::R1 + q] = dj;  // 2D: in place over this point's own grad slot
         } else {
           mn = minloc(mn, MinLoc{dj, eg * QP + q});
         }
@@ -496,27 +533,15 @@ __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const _
           if constexpr (KIND == K_ENERGY) {
             acc += wpt * metric_mu<DIM>(a.metric, tau, I1, S);
           } else if constexpr (KIND == K_SETUP) {
-            if (tmpl) {
-              constexpr int F = qfields_template<DIM>();
-              double *qo = a.qout + eg * F * QP + q;
-              double c[4];
-              metric_second_coeffs(a.metric, tau, I1, c);
-              const double sw = a.coef_h * wpt;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) qo[k * QP] = sw * c[k];
-              store_point<DIM>(qo + 4 * QP, QP, S);
-              store_point<DIM>(qo + (4 + DIM * DIM) * QP, QP, T);
-            } else {
-              constexpr int F = qfields_nt<DIM>();
-              double *qo = a.qout + eg * F * QP + q;
-              qo[0] = a.coef_h * wpt;
-              store_point<DIM>(qo + QP, QP, S);
-              store_point<DIM>(qo + (1 + DIM * DIM) * QP, QP, T);
-            }
+            // lean record (operator.py:350-371 restated; see lean_k0)
+            double *qo = a.qout + eg * QS + q;
+            store_point<DIM>(qo, QP, T);
+            qo[DIM * DIM * QP] = lean_k0(a.metric, a.coef_h * wpt, tau);
+            qo[(DIM * DIM + 1) * QP] = 1.0 / tau;
           } else {  // K_GRAD
             const double cw = a.coef_g * wpt;
             double P[DIM][DIM];
-            if (tmpl) {
+            if (metric_is_template(a.metric)) {
               double at, as;
               metric_first_coeffs(a.metric, tau, I1, at, as);
               const double ct = cw * at * a.inv_s;
@@ -538,6 +563,12 @@ __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const _
       }
     }
     __syncthreads();
+    if constexpr (APPLY) {
+      // the staging buffer is free again: stream in the next group's Q-data
+      phase ^= 1u;
+      const int64_t nxt = grp + gridDim.x;
+      if (threadIdx.x == 0 && nxt < a.ngroups) issue(nxt);
+    }
 
     if constexpr (KIND == K_ELEMDET) {
       for (int e = threadIdx.x; e < EPB; e += ELEM_NT) {
@@ -556,7 +587,7 @@ __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const _
     }
 
     // ---- backward sweeps to the element-blocked E-vector
-    if constexpr (KIND == K_APPLY || KIND == K_APPLY_NT || KIND == K_GRAD) {
+    if constexpr (APPLY || KIND == K_GRAD) {
       if constexpr (DIM == 3) {
         b3_3d<N, Q>(t, R2, R1);
         __syncthreads();
@@ -589,7 +620,7 @@ __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const _
 // ------------------------------------------------- diagonal (K_DIAG)
 // diag[(a,i)] = sum_q sum_{n,p} D_n(q,i) H[(a,n),(a,p)](q) D_p(q,i), with
 // D_n(q,i) D_p(q,i) a product of per-axis tables (Mn .* Mp) (operator.py:
-// 433-451).  One (n,p) pair at a time: point values -> 3 transposed sweeps,
+// 433-451).  One (n,p) pair at a time: point values -> transposed sweeps,
 // accumulated into the E-vector.
 template <int Q, int N>
 __device__ __forceinline__ double tprod(const Tab &t, int sel, int q, int k) {
@@ -601,8 +632,8 @@ __device__ __forceinline__ double tprod(const Tab &t, int sel, int q, int k) {
 template <int DIM, int N, int Q, bool NTM>
 __global__ void __launch_bounds__(ELEM_NT) diag_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
   using CF = Cfg<DIM, N, Q>;
-  constexpr int QP = CF::QP, NP = CF::NP, EPB = CF::EPB;
-  extern __shared__ double smem[];
+  constexpr int QP = CF::QP, NP = CF::NP, EPB = CF::EPB, QS = CF::QS;
+  extern __shared__ __align__(16) double smem[];
   double *R1 = smem;
   double *R2 = smem + EPB * CF::R1;
 
@@ -610,54 +641,48 @@ __global__ void __launch_bounds__(ELEM_NT) diag_kernel(const ElemArgs a, const _
     const int64_t e0 = grp * EPB;
     for (int n = 0; n < DIM; ++n) {
       for (int p = 0; p < DIM; ++p) {
-        // point values hv[c][q] -> R2
+        // point values hv[c][q] = H[(c,n),(c,p)] -> R2
         for (int w = threadIdx.x; w < EPB * QP; w += ELEM_NT) {
           const int e = w / QP, q = w % QP;
           const int64_t eg = e0 + e;
           double hv[DIM];
           if (eg < a.ne) {
+            const double *qd = a.qdata + eg * QS + q;
+            double T[DIM][DIM], S[DIM][DIM], k0, itau;
+            lean_load<DIM>(qd, QP, T, S, k0, itau);
             if constexpr (!NTM) {
-              constexpr int F = qfields_template<DIM>();
-              const double *qd = a.qdata + eg * F * QP + q;
-              const double c0 = qd[0], c1 = qd[QP], c23 = qd[2 * QP] + qd[3 * QP];
+              double c[4];
+              lean_coeffs(a.metric, k0, itau, mfro2<DIM>(T), c);
+              const double c23 = c[2] + c[3];
 #pragma unroll
-              for (int c = 0; c < DIM; ++c) {
-                const double sn = qd[(4 + c * DIM + n) * QP], sp = qd[(4 + c * DIM + p) * QP];
-                const double tn = qd[(4 + DIM * DIM + c * DIM + n) * QP], tp = qd[(4 + DIM * DIM + c * DIM + p) * QP];
-                double v = c1 * (sn * tp + tn * sp) + c23 * sn * sp;
-                if (n == p) v += c0;
-                hv[c] = v;
+              for (int cc = 0; cc < DIM; ++cc) {
+                const double sn = S[cc][n], sp = S[cc][p], tn = T[cc][n], tp = T[cc][p];
+                double v = c[1] * (sn * tp + tn * sp) + c23 * sn * sp;
+                if (n == p) v += c[0];
+                hv[cc] = v;
               }
             } else {
-              constexpr int F = qfields_nt<DIM>();
-              const double *qd = a.qdata + eg * F * QP + q;
-              double S[DIM][DIM], T[DIM][DIM];
-              const double wv = qd[0];
-              load_point<DIM>(qd + QP, QP, S);
-              load_point<DIM>(qd + (1 + DIM * DIM) * QP, QP, T);
 #pragma unroll
-              for (int c = 0; c < DIM; ++c) {
+              for (int cc = 0; cc < DIM; ++cc) {
                 double g[DIM][DIM] = {}, z[DIM][DIM];
-                g[c][p] = 1.0;
-                nt_hess<DIM>(a.metric, wv, S, T, g, z);
-                hv[c] = z[c][n];
+                g[cc][p] = 1.0;
+                nt_hess<DIM>(a.metric, k0, S, T, g, z);
+                hv[cc] = z[cc][n];
               }
             }
           } else {
 #pragma unroll
-            for (int c = 0; c < DIM; ++c) hv[c] = 0.0;
+            for (int cc = 0; cc < DIM; ++cc) hv[cc] = 0.0;
           }
 #pragma unroll
-          for (int c = 0; c < DIM; ++c) R2[e * CF::R2 + c * QP + q] = hv[c];
+          for (int cc = 0; cc < DIM; ++cc) R2[e * CF::R2 + cc * QP + q] = hv[cc];
         }
         __syncthreads();
-        // per-axis table selectors (axis 0 = x)
         int sel[3];
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) sel[ax] = (ax == n) + (ax == p);
         const bool first = (n == 0 && p == 0);
         if constexpr (DIM == 3) {
-          // x: R2 [c][qz][qy][qx] -> R1 [c][qz][qy][kx]
           for (int w = threadIdx.x; w < EPB * 3 * Q * Q; w += ELEM_NT) {
             const int e = w / (3 * Q * Q), r = w % (3 * Q * Q);
             const double *z = R2 + e * CF::R2 + r * Q;
@@ -671,7 +696,6 @@ __global__ void __launch_bounds__(ELEM_NT) diag_kernel(const ElemArgs a, const _
             }
           }
           __syncthreads();
-          // y: R1 [c][qz][qy][kx] -> R2 [c][qz][ky][kx]
           for (int w = threadIdx.x; w < EPB * 3 * Q * N; w += ELEM_NT) {
             const int e = w / (3 * Q * N), r = w % (3 * Q * N), cz = r / N, kx = r % N;
             const double *z = R1 + e * CF::R1 + cz * Q * N + kx;
@@ -685,7 +709,6 @@ __global__ void __launch_bounds__(ELEM_NT) diag_kernel(const ElemArgs a, const _
             }
           }
           __syncthreads();
-          // z: R2 [c][qz][ky][kx] -> E [e][c][kz][ky][kx] (accumulate)
           for (int w = threadIdx.x; w < EPB * 3 * N * N; w += ELEM_NT) {
             const int e = w / (3 * N * N), r = w % (3 * N * N), c = r / (N * N), kk = r % (N * N);
             if (e0 + e >= a.ne) continue;
@@ -700,7 +723,6 @@ __global__ void __launch_bounds__(ELEM_NT) diag_kernel(const ElemArgs a, const _
             }
           }
         } else {
-          // x: R2 [c][qy][qx] -> R1 [c][qy][kx]
           for (int w = threadIdx.x; w < EPB * 2 * Q; w += ELEM_NT) {
             const int e = w / (2 * Q), r = w % (2 * Q);
             const double *z = R2 + e * CF::R2 + r * Q;
@@ -714,7 +736,6 @@ __global__ void __launch_bounds__(ELEM_NT) diag_kernel(const ElemArgs a, const _
             }
           }
           __syncthreads();
-          // y: R1 [c][qy][kx] -> E [e][c][ky][kx]
           for (int w = threadIdx.x; w < EPB * 2 * N; w += ELEM_NT) {
             const int e = w / (2 * N), r = w % (2 * N), c = r / N, kx = r % N;
             if (e0 + e >= a.ne) continue;
@@ -733,6 +754,40 @@ __global__ void __launch_bounds__(ELEM_NT) diag_kernel(const ElemArgs a, const _
       }
     }
   }
+}
+
+// ------------------------------------------ lean -> reference Q-data
+// Materialises the reference's planar HessQData arrays (operator.py:105-113)
+// from the lean record: template metrics -> coeffs (4), S, T; non-template
+// -> w (1), S, T.  out is (fields_ref, ne * QP) planar.
+template <int D>
+__global__ void qdata_expand_kernel(int metric, int64_t ne, int QP, int QS, const double *__restrict__ qd,
+                                    double *__restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nq = ne * QP;
+  if (k >= nq) return;
+  const int64_t e = k / QP;
+  const int q = (int)(k - e * QP);
+  double T[D][D], S[D][D], k0, itau;
+  lean_load<D>(qd + e * QS + q, QP, T, S, k0, itau);
+  int f = 0;
+  if (metric_is_template(metric)) {
+    double c[4];
+    lean_coeffs(metric, k0, itau, mfro2<D>(T), c);
+    for (; f < 4; ++f) out[f * nq + k] = c[f];
+  } else {
+    out[k] = k0;
+    f = 1;
+  }
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) out[(f + i * D + j) * nq + k] = S[i][j];
+  f += D * D;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) out[(f + i * D + j) * nq + k] = T[i][j];
 }
 
 }  // namespace tmop

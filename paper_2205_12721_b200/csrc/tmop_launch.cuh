@@ -24,12 +24,13 @@ int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
   } else {
     kfn = elem_kernel<DIM, N, Q, KIND>;
   }
+  constexpr int smem = (KIND == K_APPLY || KIND == K_APPLY_NT) ? CF::SMEM_TMA : CF::SMEM;
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM) != cudaSuccess) return -2;
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -2;
     configured = true;
   }
-  kfn<<<grid, ELEM_NT, CF::SMEM, s>>>(a, t);
+  kfn<<<grid, ELEM_NT, smem, s>>>(a, t);
   return grid;
 }
 

@@ -102,16 +102,23 @@ def _is_torch(x) -> bool:
 class HessQData:
     """Partially assembled Hessian on the device (operator.py:91-138).
 
-    `data` is element-blocked: (n_elements, fields, Q) float64 with fields =
-    c_id, c_ts, c_ss, c_x, S (d*d), T (d*d) for template metrics (the
-    reference's 4 + 2 d^2 values per point) and w, S, T for mu_302 / mu_321.
-    The reference's planar arrays are materialised on demand.
+    `data` is the lean element-blocked record (n_elements, stride) float64:
+    per point T (d*d), k0, itau = 1/det T (include/tmop_b200.h) -- d^2 + 2
+    doubles per point instead of the reference's 4 + 2 d^2.  The reference's
+    planar arrays `coeffs`, `s_mat`, `t_mat` and `block(e, q)` are
+    materialised on demand by a device kernel (tmop_qdata_to_reference).
     """
     data: object
     dim: int
     n_quad_total: int
     template: bool
-    host: bool = False   # built from a numpy x: diagonal() answers in numpy
+    host: bool = False          # built from a numpy x: diagonal() answers in numpy
+    _expand: object = None      # callable(data) -> (fields_ref, NQ) device tensor
+    _ref: object = None
+
+    @property
+    def fields(self) -> int:
+        return self.dim * self.dim + 2
 
     @property
     def nbytes(self) -> int:
@@ -125,37 +132,43 @@ class HessQData:
     def bytes_per_element(self) -> int:
         return self.nbytes // max(self.n_elements, 1)
 
-    def _planar(self, lo: int, hi: int):
-        arr = self.data.permute(1, 0, 2).reshape(self.data.shape[1], -1).cpu().numpy()
-        return arr[lo:hi]
+    @property
+    def reference_nbytes(self) -> int:
+        """Bytes of the same data in the reference's HessQData format."""
+        f = (4 if self.template else 1) + 2 * self.dim * self.dim
+        return 8 * f * self.n_quad_total * self.n_elements
+
+    def _planar(self):
+        if self._ref is None:
+            self._ref = self._expand(self.data).cpu().numpy()
+        return self._ref
 
     @property
     def coeffs(self) -> np.ndarray:
         if not self.template:
-            raise AttributeError("non-template metrics store (w, S, T) per point, not coeffs")
-        return self._planar(0, 4)
+            raise AttributeError("mu_302 / mu_321 carry a point weight, not template coefficients")
+        return self._planar()[:4]
 
     @property
     def s_mat(self) -> np.ndarray:
-        o = 4 if self.template else 1
-        d = self.dim
-        return self._planar(o, o + d * d).reshape(d, d, -1)
+        o, d = (4 if self.template else 1), self.dim
+        return self._planar()[o:o + d * d].reshape(d, d, -1)
 
     @property
     def t_mat(self) -> np.ndarray:
-        o = (4 if self.template else 1) + self.dim * self.dim
         d = self.dim
-        return self._planar(o, o + d * d).reshape(d, d, -1)
+        o = (4 if self.template else 1) + d * d
+        return self._planar()[o:o + d * d].reshape(d, d, -1)
 
     def block(self, element: int, point: int) -> np.ndarray:
         """Full (d^2 x d^2) block at (element, point) (operator.py:127-138)."""
         if not self.template:
             raise NotImplementedError("block() reconstruction is defined for template metrics")
         d = self.dim
-        col = self.data[element, :, point].cpu().numpy()
-        c_id, c_ts, c_ss, c_x = col[:4]
-        sv = col[4:4 + d * d]
-        tv = col[4 + d * d:4 + 2 * d * d]
+        k = element * self.n_quad_total + point
+        c_id, c_ts, c_ss, c_x = self.coeffs[:, k]
+        sv = self.s_mat[:, :, k].ravel()
+        tv = self.t_mat[:, :, k].ravel()
         full = c_id * np.eye(d * d)
         full += c_ts * (np.outer(sv, tv) + np.outer(tv, sv))
         full += c_ss * np.outer(sv, sv)
@@ -218,6 +231,7 @@ class TmopProblem:
         self._scalar = torch.zeros(1, dtype=torch.float64, device=self.device)
         self.template = is_template_metric(config.metric)
         self.qdata_fields = self.lib.tmop_qdata_fields(ctx)
+        self.qdata_stride = int(self.lib.tmop_qdata_stride(ctx))
         if config.target.kind != 0 and config.target.h is None:
             vol = self.volume(mesh.coords.ravel())
             self.targets: TargetData = build_targets(mesh, config.target, self.rule, volume=vol)
@@ -358,15 +372,23 @@ class TmopProblem:
     def hessian_setup(self, x) -> HessQData:
         torch = _torch()
         xt, host = self._in(x)
-        qd = torch.empty((self.mesh.n_elements, self.qdata_fields, self.n_quad_total), dtype=torch.float64,
-                         device=self.device)
+        qd = torch.empty((self.mesh.n_elements, self.qdata_stride), dtype=torch.float64, device=self.device)
         _lib.check(self.lib.tmop_hessian_setup(self._ctx, _lib.ptr(xt), _lib.ptr(qd), _lib.ptr(self._status)),
                    "tmop_hessian_setup")
         self._count("setup")
         md, _ = self._det()
         self._raise_if_inverted(xt, md)
         return HessQData(data=qd, dim=self.mesh.dim, n_quad_total=self.n_quad_total, template=self.template,
-                         host=host)
+                         host=host, _expand=self._expand_qdata)
+
+    def _expand_qdata(self, data):
+        torch = _torch()
+        nf = self.lib.tmop_qdata_reference_fields(self._ctx)
+        out = torch.empty((nf, self.mesh.n_elements * self.n_quad_total), dtype=torch.float64, device=self.device)
+        self._sync_stream()
+        _lib.check(self.lib.tmop_qdata_to_reference(self._ctx, _lib.ptr(data), _lib.ptr(out)),
+                   "tmop_qdata_to_reference")
+        return out
 
     def hessian_apply(self, qdata: HessQData, v, out=None):
         """Action of the Hessian frozen at the setup positions; constrained
