@@ -51,10 +51,18 @@ template <int DIM, int N, int Q>
 struct Cfg {
   static constexpr int NP = ipow(N, DIM);
   static constexpr int QP = ipow(Q, DIM);
+  // x-lines of the W/A (length N) and grad/z (length Q) buffers are padded to
+  // an odd number of doubles: a half-warp walking consecutive lines then hits
+  // 16 distinct bank pairs (even strides caused 2- to 8-way conflicts).
+  static constexpr int NL = N | 1;
+  static constexpr int QL = Q | 1;
+  static constexpr int WF = Q * Q * NL;                       // one (c, variant) block of W / A (3D)
+  static constexpr int GF = DIM == 3 ? Q * Q * QL : Q * QL;   // one field of grad / z
   // 3D: R1 holds X / W / A (and det scratch); R2 holds U / grad+z / Bv.
   // 2D: R1 holds X / grad+z (and diag x-sweep); R2 holds U / A (and diag points).
-  static constexpr int R1 = DIM == 3 ? cmax(cmax(3 * NP, 9 * Q * Q * N), QP) : cmax(cmax(2 * NP, 4 * QP), 2 * Q * N);
-  static constexpr int R2 = DIM == 3 ? cmax(6 * Q * N * N, 9 * QP) : cmax(4 * Q * N, 2 * QP);
+  static constexpr int R1 =
+      DIM == 3 ? cmax(cmax(3 * NP, 9 * WF), QP) : cmax(cmax(2 * NP, 4 * GF), 2 * Q * N);
+  static constexpr int R2 = DIM == 3 ? cmax(6 * Q * N * N, 9 * GF) : cmax(4 * Q * NL, 2 * QP);
   static constexpr int PER = R1 + R2;
   // lean Q-data: T (d*d), k0, itau per point; element stride rounded to an
   // even number of doubles so every element block is 16-byte aligned (TMA).
@@ -146,7 +154,8 @@ __device__ __forceinline__ void f2_3d(const Tab &t, const double *R2, double *R1
     double vb[N], vg[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) { vb[k] = ub[k * N]; vg[k] = ug[k * N]; }
-    double *wb = R1 + e * CF::R1 + (c * 3) * Q * Q * N + qz * Q * N + kx;
+    constexpr int NL = CF::NL, WF = CF::WF;
+    double *wb = R1 + e * CF::R1 + (c * 3) * WF + qz * Q * NL + kx;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -156,9 +165,9 @@ __device__ __forceinline__ void f2_3d(const Tab &t, const double *R2, double *R1
         s1 += tG<Q, N>(t, q, k) * vb[k];
         s2 += tB<Q, N>(t, q, k) * vg[k];
       }
-      wb[q * N] = s0;
-      wb[Q * Q * N + q * N] = s1;
-      wb[2 * Q * Q * N + q * N] = s2;
+      wb[q * NL] = s0;
+      wb[WF + q * NL] = s1;
+      wb[2 * WF + q * NL] = s2;
     }
   }
 }
@@ -170,15 +179,16 @@ __device__ __forceinline__ void f3_3d(const Tab &t, const double *R1, double *R2
   constexpr int ITEMS = C * Q * Q, QP = Q * Q * Q;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * Q), qq = r % (Q * Q);
-    const double *wb = R1 + e * CF::R1 + (c * 3) * Q * Q * N + qq * N;
+    constexpr int WF = CF::WF, GF = CF::GF;
+    const double *wb = R1 + e * CF::R1 + (c * 3) * WF + qq * CF::NL;
     double bb[N], bg[N], gb[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       bb[k] = wb[k];
-      bg[k] = wb[Q * Q * N + k];
-      gb[k] = wb[2 * Q * Q * N + k];
+      bg[k] = wb[WF + k];
+      gb[k] = wb[2 * WF + k];
     }
-    double *g = R2 + e * CF::R2 + (c * 3) * QP + qq * Q;
+    double *g = R2 + e * CF::R2 + (c * 3) * GF + qq * CF::QL;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -189,8 +199,8 @@ __device__ __forceinline__ void f3_3d(const Tab &t, const double *R1, double *R2
         s2 += tB<Q, N>(t, q, k) * gb[k];
       }
       g[q] = s0;
-      g[QP + q] = s1;
-      g[2 * QP + q] = s2;
+      g[GF + q] = s1;
+      g[2 * GF + q] = s2;
     }
   }
 }
@@ -203,11 +213,12 @@ __device__ __forceinline__ void b3_3d(const Tab &t, const double *R2, double *R1
   constexpr int ITEMS = 3 * Q * Q, QP = Q * Q * Q;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * Q), qq = r % (Q * Q);
-    const double *z = R2 + e * CF::R2 + (c * 3) * QP + qq * Q;
+    constexpr int WF = CF::WF, GF = CF::GF;
+    const double *z = R2 + e * CF::R2 + (c * 3) * GF + qq * CF::QL;
     double z0[Q], z1[Q], z2[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) { z0[q] = z[q]; z1[q] = z[QP + q]; z2[q] = z[2 * QP + q]; }
-    double *A = R1 + e * CF::R1 + (c * 3) * Q * Q * N + qq * N;
+    for (int q = 0; q < Q; ++q) { z0[q] = z[q]; z1[q] = z[GF + q]; z2[q] = z[2 * GF + q]; }
+    double *A = R1 + e * CF::R1 + (c * 3) * WF + qq * CF::NL;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -218,8 +229,8 @@ __device__ __forceinline__ void b3_3d(const Tab &t, const double *R2, double *R1
         s2 += tB<Q, N>(t, q, k) * z2[q];
       }
       A[k] = s0;
-      A[Q * Q * N + k] = s1;
-      A[2 * Q * Q * N + k] = s2;
+      A[WF + k] = s1;
+      A[2 * WF + k] = s2;
     }
   }
 }
@@ -231,13 +242,14 @@ __device__ __forceinline__ void b2_3d(const Tab &t, const double *R1, double *R2
   constexpr int ITEMS = 3 * Q * N;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * N), r2 = r % (Q * N), qz = r2 / N, kx = r2 % N;
-    const double *A = R1 + e * CF::R1 + (c * 3) * Q * Q * N + qz * Q * N + kx;
+    constexpr int NL = CF::NL, WF = CF::WF;
+    const double *A = R1 + e * CF::R1 + (c * 3) * WF + qz * Q * NL + kx;
     double a0[Q], a1[Q], a2[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      a0[q] = A[q * N];
-      a1[q] = A[Q * Q * N + q * N];
-      a2[q] = A[2 * Q * Q * N + q * N];
+      a0[q] = A[q * NL];
+      a1[q] = A[WF + q * NL];
+      a2[q] = A[2 * WF + q * NL];
     }
     double *b = R2 + e * CF::R2 + (c * 2) * Q * N * N + qz * N * N + kx;
 #pragma unroll
@@ -290,7 +302,8 @@ __device__ __forceinline__ void f1_2d(const Tab &t, const double *R1, double *R2
     double xv[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) xv[k] = x[k * N];
-    double *u = R2 + e * CF::R2 + c * 2 * Q * N + kx;
+    constexpr int NL = CF::NL;
+    double *u = R2 + e * CF::R2 + c * 2 * Q * NL + kx;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       double sb = 0.0, sg = 0.0;
@@ -299,8 +312,8 @@ __device__ __forceinline__ void f1_2d(const Tab &t, const double *R1, double *R2
         sb += tB<Q, N>(t, q, k) * xv[k];
         sg += tG<Q, N>(t, q, k) * xv[k];
       }
-      u[q * N] = sb;
-      u[Q * N + q * N] = sg;
+      u[q * NL] = sb;
+      u[Q * NL + q * NL] = sg;
     }
   }
 }
@@ -312,12 +325,13 @@ __device__ __forceinline__ void f2_2d(const Tab &t, const double *R2, double *G)
   constexpr int ITEMS = C * Q, QP = Q * Q;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / Q, qy = r % Q;
-    const double *ub = R2 + e * CF::R2 + (c * 2) * Q * N + qy * N;
-    const double *ug = ub + Q * N;
+    constexpr int NL = CF::NL, GF = CF::GF;
+    const double *ub = R2 + e * CF::R2 + (c * 2) * Q * NL + qy * NL;
+    const double *ug = ub + Q * NL;
     double vb[N], vg[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) { vb[k] = ub[k]; vg[k] = ug[k]; }
-    double *g = G + e * CF::R1 + (c * 2) * QP + qy * Q;
+    double *g = G + e * CF::R1 + (c * 2) * GF + qy * CF::QL;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       double s0 = 0.0, s1 = 0.0;
@@ -327,7 +341,7 @@ __device__ __forceinline__ void f2_2d(const Tab &t, const double *R2, double *G)
         s1 += tB<Q, N>(t, q, k) * vg[k];
       }
       g[q] = s0;
-      g[QP + q] = s1;
+      g[GF + q] = s1;
     }
   }
 }
@@ -339,11 +353,12 @@ __device__ __forceinline__ void b2_2d(const Tab &t, const double *Z, double *R2)
   constexpr int ITEMS = 2 * Q, QP = Q * Q;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / Q, qy = r % Q;
-    const double *z = Z + e * CF::R1 + (c * 2) * QP + qy * Q;
+    constexpr int NL = CF::NL, GF = CF::GF;
+    const double *z = Z + e * CF::R1 + (c * 2) * GF + qy * CF::QL;
     double z0[Q], z1[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) { z0[q] = z[q]; z1[q] = z[QP + q]; }
-    double *A = R2 + e * CF::R2 + (c * 2) * Q * N + qy * N;
+    for (int q = 0; q < Q; ++q) { z0[q] = z[q]; z1[q] = z[GF + q]; }
+    double *A = R2 + e * CF::R2 + (c * 2) * Q * NL + qy * NL;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       double s0 = 0.0, s1 = 0.0;
@@ -353,7 +368,7 @@ __device__ __forceinline__ void b2_2d(const Tab &t, const double *Z, double *R2)
         s1 += tB<Q, N>(t, q, k) * z1[q];
       }
       A[k] = s0;
-      A[Q * N + k] = s1;
+      A[Q * NL + k] = s1;
     }
   }
 }
@@ -367,10 +382,11 @@ __device__ __forceinline__ void b1_2d(const Tab &t, const double *R2, double *__
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / N, kx = r % N;
     if (e0 + e >= ne) continue;
-    const double *A = R2 + e * CF::R2 + (c * 2) * Q * N + kx;
+    constexpr int NL = CF::NL;
+    const double *A = R2 + e * CF::R2 + (c * 2) * Q * NL + kx;
     double a0[Q], a1[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) { a0[q] = A[q * N]; a1[q] = A[Q * N + q * N]; }
+    for (int q = 0; q < Q; ++q) { a0[q] = A[q * NL]; a1[q] = A[Q * NL + q * NL]; }
     double *out = E + ((e0 + e) * 2 + c) * NP + kx;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -497,21 +513,22 @@ __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const _
       const int e = w / QP, q = w % QP;
       const int64_t eg = e0 + e;
       if (eg >= a.ne) continue;
-      double *gp = Gp + e * gstride + q;
+      const int gi = (q / Q) * CF::QL + q % Q;   // padded x-line index of the point
+      double *gp = Gp + e * gstride + gi;
       double A[DIM][DIM];
-      load_point<DIM>(gp, QP, A);
+      load_point<DIM>(gp, CF::GF, A);
 
       if constexpr (APPLY) {
         double z[DIM][DIM];
         lean_hess<DIM, KIND == K_APPLY_NT>(a.metric, QB + e * QS + q, QP, A, z);
-        store_point<DIM>(gp, QP, z);
+        store_point<DIM>(gp, CF::GF, z);
       } else {
         // A is the Jacobian dx/dxi at the point
         const double dj = mdet<DIM>(A);
         if constexpr (KIND == K_VOLUME) {
           acc += dj * wq<DIM, Q>(t, q);
         } else if constexpr (KIND == K_ELEMDET) {
-          R1[e * CF::R1 + q] = dj;  // 2D: in place over this point's own grad slot
+          R1[e * CF::R1 + gi] = dj;  // own field-0 slot (2D: in place over this point's grad)
         } else {
           mn = minloc(mn, MinLoc{dj, eg * QP + q});
         }
@@ -557,7 +574,7 @@ __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const _
 #pragma unroll
                 for (int j = 0; j < DIM; ++j) P[i][j] *= cw;
             }
-            store_point<DIM>(gp, QP, P);
+            store_point<DIM>(gp, CF::GF, P);
           }
         }
       }
@@ -577,7 +594,7 @@ __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const _
         double m = R1[e * CF::R1];
         int arg = 0;
         for (int q = 1; q < QP; ++q) {
-          const double v = R1[e * CF::R1 + q];
+          const double v = R1[e * CF::R1 + (q / Q) * CF::QL + q % Q];
           if (v < m) { m = v; arg = q; }
         }
         a.elem_min[eg] = m;

@@ -5,14 +5,48 @@
 
 #include <algorithm>
 
+#include <cstdlib>
+#include <cstring>
+
+#include "tmop_apply_col.cuh"
 #include "tmop_elem.cuh"
 #include "tmop_internal.h"
 
 namespace tmop {
 
+// TMOP_APPLY_KERNEL=generic selects the work-item kernel for the Hessian
+// action instead of the column kernel (A/B measurements).
+inline bool use_generic_apply() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = std::getenv("TMOP_APPLY_KERNEL");
+    v = (e && std::strcmp(e, "generic") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <int N, int Q, bool NTM>
+int launch_col(ElemArgs &a, const Tab &t, cudaStream_t s) {
+  using CC = ColCfg<N, Q>;
+  a.ngroups = (a.ne + CC::E - 1) / CC::E;
+  const int grid = (int)std::min<int64_t>(a.ngroups, GRID_CAP);
+  if (grid == 0) return 0;
+  auto kfn = apply_col_kernel<N, Q, NTM>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM) != cudaSuccess) return -2;
+    configured = true;
+  }
+  kfn<<<grid, CC::NT, CC::SMEM, s>>>(a, t);
+  return grid;
+}
+
 template <int DIM, int N, int Q, int KIND>
 int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
   using CF = Cfg<DIM, N, Q>;
+  if constexpr (DIM == 3 && (KIND == K_APPLY || KIND == K_APPLY_NT) && col_supported<N, Q>()) {
+    if (!use_generic_apply()) return launch_col<N, Q, KIND == K_APPLY_NT>(a, t, s);
+  }
   a.ngroups = (a.ne + CF::EPB - 1) / CF::EPB;
   const int grid = (int)std::min<int64_t>(a.ngroups, GRID_CAP);
   if (grid == 0) return 0;
