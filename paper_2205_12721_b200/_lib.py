@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtmop_b200.so")
+LIB_PATH = os.environ.get("TMOP_LIB", os.path.join(_HERE, "libtmop_b200.so"))
 
 TMOP_OK = 0
 

@@ -40,8 +40,19 @@ enum Kind : int {
   K_COUNT = 10
 };
 
+// Tuning knobs (compile-time; see tools/build_variant.sh): threads per CTA,
+// shared-memory budget per CTA in doubles, and the occupancy hint.
+#ifndef TMOP_ELEM_NT
+#define TMOP_ELEM_NT 256
+#endif
+#ifndef TMOP_SMEM_BUDGET
+#define TMOP_SMEM_BUDGET 14336
+#endif
+#ifndef TMOP_MIN_BLOCKS
+#define TMOP_MIN_BLOCKS 1
+#endif
 constexpr int GRID_CAP = 148 * 8;
-constexpr int ELEM_NT = 256;
+constexpr int ELEM_NT = TMOP_ELEM_NT;
 
 __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -69,7 +80,7 @@ struct Cfg {
   static constexpr int F = DIM * DIM + 2;
   static constexpr int QS = (F * QP + 1) & ~1;
   // elements per CTA: work arrays + staged Q-data in ~112 KB (2 CTAs / SM)
-  static constexpr int EPB = cclamp(14336 / (PER + QS), 1, 32);
+  static constexpr int EPB = cclamp(TMOP_SMEM_BUDGET / (PER + QS), 1, 32);
   static constexpr int QOFF = (EPB * PER + 1) & ~1;          // Q-data staging offset (doubles)
   static constexpr int SMEM = EPB * PER * 8;                 // kernels without staging
   static constexpr int SMEM_TMA = (QOFF + EPB * QS) * 8;     // Hessian-action kernels
@@ -447,7 +458,7 @@ __device__ __forceinline__ void lean_hess(int metric, const double *qd, int QP, 
 
 // ------------------------------------------------------ the kernel
 template <int DIM, int N, int Q, int KIND>
-__global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
+__global__ void __launch_bounds__(ELEM_NT, TMOP_MIN_BLOCKS) elem_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
   using CF = Cfg<DIM, N, Q>;
   constexpr int QP = CF::QP, EPB = CF::EPB, QS = CF::QS;
   constexpr bool APPLY = (KIND == K_APPLY || KIND == K_APPLY_NT);
@@ -630,145 +641,6 @@ __global__ void __launch_bounds__(ELEM_NT) elem_kernel(const ElemArgs a, const _
     if (threadIdx.x == 0) {
       a.part_min[blockIdx.x] = m.v;
       a.part_arg[blockIdx.x] = m.i;
-    }
-  }
-}
-
-// ------------------------------------------------- diagonal (K_DIAG)
-// diag[(a,i)] = sum_q sum_{n,p} D_n(q,i) H[(a,n),(a,p)](q) D_p(q,i), with
-// D_n(q,i) D_p(q,i) a product of per-axis tables (Mn .* Mp) (operator.py:
-// 433-451).  One (n,p) pair at a time: point values -> transposed sweeps,
-// accumulated into the E-vector.
-template <int Q, int N>
-__device__ __forceinline__ double tprod(const Tab &t, int sel, int q, int k) {
-  // sel: 0 = B.B, 1 = B.G, 2 = G.G
-  const double b = tB<Q, N>(t, q, k), g = tG<Q, N>(t, q, k);
-  return sel == 0 ? b * b : (sel == 1 ? b * g : g * g);
-}
-
-template <int DIM, int N, int Q, bool NTM>
-__global__ void __launch_bounds__(ELEM_NT) diag_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
-  using CF = Cfg<DIM, N, Q>;
-  constexpr int QP = CF::QP, NP = CF::NP, EPB = CF::EPB, QS = CF::QS;
-  extern __shared__ __align__(16) double smem[];
-  double *R1 = smem;
-  double *R2 = smem + EPB * CF::R1;
-
-  for (int64_t grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
-    const int64_t e0 = grp * EPB;
-    for (int n = 0; n < DIM; ++n) {
-      for (int p = 0; p < DIM; ++p) {
-        // point values hv[c][q] = H[(c,n),(c,p)] -> R2
-        for (int w = threadIdx.x; w < EPB * QP; w += ELEM_NT) {
-          const int e = w / QP, q = w % QP;
-          const int64_t eg = e0 + e;
-          double hv[DIM];
-          if (eg < a.ne) {
-            const double *qd = a.qdata + eg * QS + q;
-            double T[DIM][DIM], S[DIM][DIM], k0, itau;
-            lean_load<DIM>(qd, QP, T, S, k0, itau);
-            if constexpr (!NTM) {
-              double c[4];
-              lean_coeffs(a.metric, k0, itau, mfro2<DIM>(T), c);
-              const double c23 = c[2] + c[3];
-#pragma unroll
-              for (int cc = 0; cc < DIM; ++cc) {
-                const double sn = S[cc][n], sp = S[cc][p], tn = T[cc][n], tp = T[cc][p];
-                double v = c[1] * (sn * tp + tn * sp) + c23 * sn * sp;
-                if (n == p) v += c[0];
-                hv[cc] = v;
-              }
-            } else {
-#pragma unroll
-              for (int cc = 0; cc < DIM; ++cc) {
-                double g[DIM][DIM] = {}, z[DIM][DIM];
-                g[cc][p] = 1.0;
-                nt_hess<DIM>(a.metric, k0, S, T, g, z);
-                hv[cc] = z[cc][n];
-              }
-            }
-          } else {
-#pragma unroll
-            for (int cc = 0; cc < DIM; ++cc) hv[cc] = 0.0;
-          }
-#pragma unroll
-          for (int cc = 0; cc < DIM; ++cc) R2[e * CF::R2 + cc * QP + q] = hv[cc];
-        }
-        __syncthreads();
-        int sel[3];
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) sel[ax] = (ax == n) + (ax == p);
-        const bool first = (n == 0 && p == 0);
-        if constexpr (DIM == 3) {
-          for (int w = threadIdx.x; w < EPB * 3 * Q * Q; w += ELEM_NT) {
-            const int e = w / (3 * Q * Q), r = w % (3 * Q * Q);
-            const double *z = R2 + e * CF::R2 + r * Q;
-            double *o = R1 + e * CF::R1 + r * N;
-#pragma unroll
-            for (int k = 0; k < N; ++k) {
-              double s = 0.0;
-#pragma unroll
-              for (int q = 0; q < Q; ++q) s += tprod<Q, N>(t, sel[0], q, k) * z[q];
-              o[k] = s;
-            }
-          }
-          __syncthreads();
-          for (int w = threadIdx.x; w < EPB * 3 * Q * N; w += ELEM_NT) {
-            const int e = w / (3 * Q * N), r = w % (3 * Q * N), cz = r / N, kx = r % N;
-            const double *z = R1 + e * CF::R1 + cz * Q * N + kx;
-            double *o = R2 + e * CF::R2 + cz * N * N + kx;
-#pragma unroll
-            for (int k = 0; k < N; ++k) {
-              double s = 0.0;
-#pragma unroll
-              for (int q = 0; q < Q; ++q) s += tprod<Q, N>(t, sel[1], q, k) * z[q * N];
-              o[k * N] = s;
-            }
-          }
-          __syncthreads();
-          for (int w = threadIdx.x; w < EPB * 3 * N * N; w += ELEM_NT) {
-            const int e = w / (3 * N * N), r = w % (3 * N * N), c = r / (N * N), kk = r % (N * N);
-            if (e0 + e >= a.ne) continue;
-            const double *z = R2 + e * CF::R2 + c * Q * N * N + kk;
-            double *o = a.E + ((e0 + e) * 3 + c) * NP + kk;
-#pragma unroll
-            for (int k = 0; k < N; ++k) {
-              double s = 0.0;
-#pragma unroll
-              for (int q = 0; q < Q; ++q) s += tprod<Q, N>(t, sel[2], q, k) * z[q * N * N];
-              o[k * N * N] = first ? s : o[k * N * N] + s;
-            }
-          }
-        } else {
-          for (int w = threadIdx.x; w < EPB * 2 * Q; w += ELEM_NT) {
-            const int e = w / (2 * Q), r = w % (2 * Q);
-            const double *z = R2 + e * CF::R2 + r * Q;
-            double *o = R1 + e * CF::R1 + r * N;
-#pragma unroll
-            for (int k = 0; k < N; ++k) {
-              double s = 0.0;
-#pragma unroll
-              for (int q = 0; q < Q; ++q) s += tprod<Q, N>(t, sel[0], q, k) * z[q];
-              o[k] = s;
-            }
-          }
-          __syncthreads();
-          for (int w = threadIdx.x; w < EPB * 2 * N; w += ELEM_NT) {
-            const int e = w / (2 * N), r = w % (2 * N), c = r / N, kx = r % N;
-            if (e0 + e >= a.ne) continue;
-            const double *z = R1 + e * CF::R1 + c * Q * N + kx;
-            double *o = a.E + ((e0 + e) * 2 + c) * NP + kx;
-#pragma unroll
-            for (int k = 0; k < N; ++k) {
-              double s = 0.0;
-#pragma unroll
-              for (int q = 0; q < Q; ++q) s += tprod<Q, N>(t, sel[1], q, k) * z[q * N];
-              o[k * N] = first ? s : o[k * N] + s;
-            }
-          }
-        }
-        __syncthreads();
-      }
     }
   }
 }

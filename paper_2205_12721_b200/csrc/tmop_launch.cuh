@@ -9,6 +9,7 @@
 #include <cstring>
 
 #include "tmop_apply_col.cuh"
+#include "tmop_diag.cuh"
 #include "tmop_elem.cuh"
 #include "tmop_internal.h"
 
@@ -41,31 +42,44 @@ int launch_col(ElemArgs &a, const Tab &t, cudaStream_t s) {
   return grid;
 }
 
+template <int DIM, int N, int Q, bool NTM>
+int launch_diag(ElemArgs &a, const Tab &t, cudaStream_t s) {
+  using DC = DiagCfg<DIM, N, Q>;
+  a.ngroups = (a.ne + DC::EPB - 1) / DC::EPB;
+  const int grid = (int)std::min<int64_t>(a.ngroups, GRID_CAP);
+  if (grid == 0) return 0;
+  auto kfn = diag2_kernel<DIM, N, Q, NTM>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, DC::SMEM) != cudaSuccess) return -2;
+    configured = true;
+  }
+  kfn<<<grid, ELEM_NT, DC::SMEM, s>>>(a, t);
+  return grid;
+}
+
 template <int DIM, int N, int Q, int KIND>
 int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
   using CF = Cfg<DIM, N, Q>;
-  if constexpr (DIM == 3 && (KIND == K_APPLY || KIND == K_APPLY_NT) && col_supported<N, Q>()) {
-    if (!use_generic_apply()) return launch_col<N, Q, KIND == K_APPLY_NT>(a, t, s);
-  }
-  a.ngroups = (a.ne + CF::EPB - 1) / CF::EPB;
-  const int grid = (int)std::min<int64_t>(a.ngroups, GRID_CAP);
-  if (grid == 0) return 0;
-  void (*kfn)(const ElemArgs, const Tab);
-  if constexpr (KIND == K_DIAG) {
-    kfn = diag_kernel<DIM, N, Q, false>;
-  } else if constexpr (KIND == K_DIAG_NT) {
-    kfn = diag_kernel<DIM, N, Q, true>;
+  if constexpr (KIND == K_DIAG || KIND == K_DIAG_NT) {
+    return launch_diag<DIM, N, Q, KIND == K_DIAG_NT>(a, t, s);
   } else {
-    kfn = elem_kernel<DIM, N, Q, KIND>;
+    if constexpr (DIM == 3 && (KIND == K_APPLY || KIND == K_APPLY_NT) && col_supported<N, Q>()) {
+      if (!use_generic_apply()) return launch_col<N, Q, KIND == K_APPLY_NT>(a, t, s);
+    }
+    a.ngroups = (a.ne + CF::EPB - 1) / CF::EPB;
+    const int grid = (int)std::min<int64_t>(a.ngroups, GRID_CAP);
+    if (grid == 0) return 0;
+    auto kfn = elem_kernel<DIM, N, Q, KIND>;
+    constexpr int smem = (KIND == K_APPLY || KIND == K_APPLY_NT) ? CF::SMEM_TMA : CF::SMEM;
+    static bool configured = false;
+    if (!configured) {
+      if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -2;
+      configured = true;
+    }
+    kfn<<<grid, ELEM_NT, smem, s>>>(a, t);
+    return grid;
   }
-  constexpr int smem = (KIND == K_APPLY || KIND == K_APPLY_NT) ? CF::SMEM_TMA : CF::SMEM;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -2;
-    configured = true;
-  }
-  kfn<<<grid, ELEM_NT, smem, s>>>(a, t);
-  return grid;
 }
 
 template <int DIM, int N, int Q>

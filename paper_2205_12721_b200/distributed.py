@@ -1,0 +1,334 @@
+"""Element-partitioned multi-GPU TMOP operator.
+
+The reference has no distributed mode (the paper's MPI operator
+P "degenerates to identity"); the paper's production code partitions
+elements across MPI ranks and assembles with P^T.  Here:
+
+* partition: z-slabs of element layers of a `build_box` lattice.  Element ids
+  and node ids are x-fastest with z slowest (mesh.py:131-156), so a slab of
+  layers [z0, z1) owns a contiguous element range and a contiguous node range;
+  consecutive slabs share one node plane.
+* exchange: after every local E->L sum (Hessian action, gradient, diagonal)
+  each rank adds the partial sums of its neighbours' copies of the shared
+  plane (one send/recv pair per neighbour, batched) -- the only data-path
+  collective.  Both copies then hold the same value (a + b == b + a
+  bitwise), so the partition needs no ownership for the vectors themselves.
+* scalars: energy SUM, min det MIN, and dot products over OWNED nodes (each
+  shared plane is owned by the lower rank) with an all-reduce SUM.
+
+The same code runs on NCCL with CUDA tensors (one process per GPU) and on
+gloo with CPU tensors (the world-size-2 tests in tests/test_distributed.py,
+where the local operator is the CPU oracle).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from .mesh import Mesh, build_box
+
+__all__ = ["SlabPartition", "HaloExchange", "DistributedProblem", "split_layers"]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def split_layers(nz: int, world: int):
+    """Element-layer ranges [z0, z1) per rank, as even as possible."""
+    if world > nz:
+        raise ValueError(f"cannot split {nz} element layers over {world} ranks")
+    base, extra = divmod(nz, world)
+    out, z = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append((z, z + n))
+        z += n
+    return out
+
+
+@dataclass
+class SlabPartition:
+    counts: tuple
+    order: int
+    world: int
+    rank: int
+
+    def __post_init__(self):
+        nx, ny, nz = self.counts
+        self.z0, self.z1 = split_layers(nz, self.world)[self.rank]
+        p = self.order
+        self.plane = (nx * p + 1) * (ny * p + 1)
+        self.node_lo = self.z0 * p * self.plane
+        self.node_hi = (self.z1 * p + 1) * self.plane
+        self.elem_lo = self.z0 * nx * ny
+        self.elem_hi = self.z1 * nx * ny
+        self.has_lower = self.rank > 0
+        self.has_upper = self.rank < self.world - 1
+        self.n_local = self.node_hi - self.node_lo
+        # owned nodes: [0, n_owned); the top plane belongs to the upper rank's
+        # bottom plane and is owned by THIS rank only if there is no upper rank
+        self.n_owned = self.n_local - self.plane if self.has_upper else self.n_local
+
+    @property
+    def local_counts(self):
+        nx, ny, _ = self.counts
+        return (nx, ny, self.z1 - self.z0)
+
+    def local_mesh(self, global_mesh: Mesh) -> Mesh:
+        """Exact slab of a global mesh: local lattice structure, global
+        coordinates and global constraint masks (interior slab faces free)."""
+        loc = build_box(3, self.local_counts, self.order)
+        sl = slice(self.node_lo, self.node_hi)
+        return replace(loc, coords=global_mesh.coords[:, sl].copy(), fixed_mask=global_mesh.fixed_mask[:, sl].copy())
+
+    def local_mesh_direct(self) -> Mesh:
+        """The same slab built without the global mesh (for large weak-scaling
+        runs): z mapped into [z0, z1] / nz and the z-faces constrained only on
+        the global boundary."""
+        nx, ny, nz = self.counts
+        loc = build_box(3, self.local_counts, self.order)
+        coords = loc.coords.copy()
+        coords[2] = (coords[2] * (self.z1 - self.z0) + self.z0) / nz
+        fixed = loc.fixed_mask.copy()
+        zl = np.arange(loc.n_nodes) // self.plane
+        top = zl == zl.max()
+        bot = zl == 0
+        fixed[2] = (bot & (not self.has_lower)) | (top & (not self.has_upper))
+        return replace(loc, coords=coords, fixed_mask=fixed)
+
+    def local_vector(self, global_vec):
+        d = 3
+        g = np.asarray(global_vec).reshape(d, -1)
+        return g[:, self.node_lo:self.node_hi].copy().ravel()
+
+    def owned_slice(self):
+        return slice(0, self.n_owned)
+
+
+class HaloExchange:
+    """Sum of the shared node planes with the z-neighbours (torch.distributed
+    point-to-point, batched; NCCL on GPUs, gloo on CPUs)."""
+
+    def __init__(self, part: SlabPartition, group=None):
+        self.part = part
+        self.group = group
+        self.bytes_per_exchange = 0
+        self.seconds = 0.0
+
+    def sum_planes(self, y):
+        """y: local T-vector (3 * n_local); the bottom / top planes receive the
+        neighbour's partial sums (in place)."""
+        torch = _torch()
+        import torch.distributed as dist
+        pt = self.part
+        y2 = y.view(3, pt.n_local)
+        ops, recv = [], []
+        pl = pt.plane
+        if pt.has_lower:
+            send_lo = y2[:, :pl].contiguous()
+            recv_lo = torch.empty_like(send_lo)
+            ops += [dist.P2POp(dist.isend, send_lo, pt.rank - 1, self.group),
+                    dist.P2POp(dist.irecv, recv_lo, pt.rank - 1, self.group)]
+            recv.append(("lo", recv_lo))
+        if pt.has_upper:
+            send_hi = y2[:, pt.n_local - pl:].contiguous()
+            recv_hi = torch.empty_like(send_hi)
+            ops += [dist.P2POp(dist.isend, send_hi, pt.rank + 1, self.group),
+                    dist.P2POp(dist.irecv, recv_hi, pt.rank + 1, self.group)]
+            recv.append(("hi", recv_hi))
+        if not ops:
+            return y
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        for side, buf in recv:
+            if side == "lo":
+                y2[:, :pl] += buf
+            else:
+                y2[:, pt.n_local - pl:] += buf
+            self.bytes_per_exchange = buf.numel() * buf.element_size()
+        return y
+
+    def refix(self, y, fixed2, value):
+        """Re-apply the constrained-dof convention on the shared planes after
+        the sum (both partial copies carried it): value is a local tensor
+        (apply: v) or a float (diagonal: 1.0)."""
+        pt = self.part
+        y2 = y.view(3, pt.n_local)
+        pl = pt.plane
+        sides = []
+        if pt.has_lower:
+            sides.append(slice(0, pl))
+        if pt.has_upper:
+            sides.append(slice(pt.n_local - pl, pt.n_local))
+        for sl in sides:
+            m = fixed2[:, sl]
+            if isinstance(value, float):
+                y2[:, sl] = y2[:, sl].masked_fill(m, value)
+            else:
+                v2 = value.view(3, pt.n_local)
+                y2[:, sl] = y2[:, sl].where(~m, v2[:, sl])
+        return y
+
+
+class DistributedProblem:
+    """`ProblemLike` over a slab partition: a local operator (the device
+    TmopProblem, or for CPU tests the oracle) + halo sums + all-reduces."""
+
+    def __init__(self, local, part: SlabPartition, fixed_mask, group=None, to_local=None, from_local=None):
+        torch = _torch()
+        self.local = local
+        self.part = part
+        self.group = group
+        self.halo = HaloExchange(part, group)
+        self.fixed2 = torch.as_tensor(np.ascontiguousarray(fixed_mask)).reshape(3, part.n_local)
+        # adapters between torch tensors and the local operator's currency
+        self._to = to_local or (lambda t: t)
+        self._from = from_local or (lambda a: a)
+
+    def _reduce(self, value: float, op):
+        torch = _torch()
+        import torch.distributed as dist
+        dev = self.fixed2.device
+        t = torch.tensor([value], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=op, group=self.group)
+        return float(t.item())
+
+    def to(self, device):
+        self.fixed2 = self.fixed2.to(device)
+        return self
+
+    # -------------------------------------------------------- ProblemLike
+    def objective(self, x) -> float:
+        import torch.distributed as dist
+        return self._reduce(self.local.objective(self._to(x)), dist.ReduceOp.SUM)
+
+    def min_det_jacobian(self, x) -> float:
+        import torch.distributed as dist
+        return self._reduce(self.local.min_det_jacobian(self._to(x)), dist.ReduceOp.MIN)
+
+    def gradient(self, x):
+        g = self._from(self.local.gradient(self._to(x)))
+        return self.halo.sum_planes(g)           # constrained entries: 0 + 0
+
+    def hessian_setup(self, x):
+        return self.local.hessian_setup(self._to(x))
+
+    def hessian_apply(self, qdata, v):
+        y = self._from(self.local.hessian_apply(qdata, self._to(v)))
+        self.halo.sum_planes(y)
+        return self.halo.refix(y, self.fixed2, v)
+
+    def hessian_diagonal(self, qdata):
+        d = self._from(self.local.hessian_diagonal(qdata))
+        self.halo.sum_planes(d)
+        return self.halo.refix(d, self.fixed2, 1.0)
+
+    def dot(self, a, b) -> float:
+        """Global dot product over owned nodes (each shared plane once)."""
+        import torch.distributed as dist
+        pt = self.part
+        a2 = a.view(3, pt.n_local)[:, :pt.n_owned]
+        b2 = b.view(3, pt.n_local)[:, :pt.n_owned]
+        return self._reduce(float((a2 * b2).sum()), dist.ReduceOp.SUM)
+
+
+# ------------------------------------------------------------------ solvers
+def dist_minres(problem: DistributedProblem, apply_op, b, max_iterations=50, rel_tolerance=1e-8, inv=None):
+    """Paige-Saunders preconditioned MINRES (solvers.py:93-180) over a slab
+    partition: vectors are local (shared planes duplicated and kept equal),
+    inner products are owned-node dots all-reduced across ranks.  Returns
+    (x, iterations, rel_residual, converged)."""
+    torch = _torch()
+    M = (lambda r: inv * r) if inv is not None else (lambda r: r)
+    x = torch.zeros_like(b)
+    r1 = b.clone()
+    y = M(r1)
+    beta1 = problem.dot(r1, y)
+    if beta1 < 0:
+        raise ValueError("preconditioner is not positive definite")
+    beta1 = float(np.sqrt(beta1))
+    if beta1 == 0.0:
+        return x, 0, 0.0, True
+    oldb, beta, dbar, epsln, sn, cs, phibar = 0.0, beta1, 0.0, 0.0, 0.0, -1.0, beta1
+    w = torch.zeros_like(b)
+    w2 = torch.zeros_like(b)
+    r2 = r1.clone()
+    itn, relres = 0, 1.0
+    while itn < max_iterations:
+        itn += 1
+        v = y / beta
+        y = apply_op(v)
+        if itn >= 2:
+            y = y - (beta / oldb) * r1
+        alfa = problem.dot(v, y)
+        y = y - (alfa / beta) * r2
+        r1, r2 = r2, y
+        y = M(r2)
+        oldb = beta
+        beta2 = problem.dot(r2, y)
+        if beta2 < 0:
+            raise ValueError("preconditioner is not positive definite")
+        beta = float(np.sqrt(beta2))
+        oldeps = epsln
+        delta = cs * dbar + sn * alfa
+        gbar = sn * dbar - cs * alfa
+        epsln = sn * beta
+        dbar = -cs * beta
+        gamma = max(float(np.hypot(gbar, beta)), float(np.finfo(float).eps))
+        cs, sn = gbar / gamma, beta / gamma
+        phi = cs * phibar
+        phibar = sn * phibar
+        w1, w2 = w2, w
+        w = (v - oldeps * w1 - delta * w2) / gamma
+        x = x + phi * w
+        relres = phibar / beta1
+        if beta == 0.0 or relres <= rel_tolerance:
+            break
+    return x, itn, relres, relres <= rel_tolerance
+
+
+def dist_newton_solve(problem: DistributedProblem, x0, max_iterations=100, rel_grad_tolerance=1e-10,
+                      minres_max=50, minres_rtol=1e-8, preconditioned=True, max_halvings=30,
+                      abs_grad_tolerance=1e-12):
+    """Newton + MINRES + line search (solvers.py:202-321) over the partition.
+    Returns (x, records, success, message); records as in SolveTrace."""
+    x = x0.clone()
+    if problem.min_det_jacobian(x) <= 0.0:
+        raise RuntimeError("initial mesh is inverted")
+    g = problem.gradient(x)
+    ng0 = float(np.sqrt(problem.dot(g, g)))
+    if ng0 <= abs_grad_tolerance:
+        return x, [], True, "initial gradient is zero"
+    f, ng, recs = problem.objective(x), ng0, []
+    for _ in range(max_iterations):
+        qd = problem.hessian_setup(x)
+        inv = None
+        if preconditioned:
+            d = problem.hessian_diagonal(qd)
+            inv = 1.0 / d.abs().clamp_min(1e-12)
+        dx, its, rr, _ = dist_minres(problem, lambda v: problem.hessian_apply(qd, v), g, minres_max,
+                                     minres_rtol, inv)
+        alpha, accepted = 1.0, False
+        for _ in range(max_halvings + 1):
+            xt = x - alpha * dx
+            md = problem.min_det_jacobian(xt)
+            if md > 0.0:
+                ft = problem.objective(xt)
+                if ft < 1.2 * f:
+                    gt = problem.gradient(xt)
+                    ngt = float(np.sqrt(problem.dot(gt, gt)))
+                    if ngt < 1.2 * ng:
+                        accepted = True
+                        break
+            alpha *= 0.5
+        if not accepted:
+            return x, recs, False, "line search failed"
+        x, f, ng, g = xt, ft, ngt, gt
+        recs.append((alpha, f, ng, its, rr, md))
+        if ng / ng0 <= rel_grad_tolerance:
+            return x, recs, True, "converged"
+    return x, recs, False, f"no convergence in {max_iterations} iterations"

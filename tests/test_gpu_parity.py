@@ -173,15 +173,17 @@ def test_properties_at_larger_size(rng):
     assert float((Hv - fd).norm() / fd.norm()) <= 1e-5
 
 
-@pytest.mark.parametrize("name,xtol,its", [("minres_wellcond", 1e-10, 12), ("minres_dense", 1e-3, 25)])
-def test_minres_matches_reference(name, xtol, its):
+@pytest.mark.parametrize("name,xtol,htol,its", [("minres_wellcond", 1e-10, 1e-10, 12),
+                                                ("minres_dense", 1e-3, 5e-2, 25)])
+def test_minres_matches_reference(name, xtol, htol, its):
     """minres_wellcond: 12 iterations on a conditioned indefinite system, where
     rounding barely amplifies (a 1e-16 perturbation of A moves x by 2e-13;
     cuBLAS dgemv + fixed-order device dots land at ~4e-12): the solver-level
     tolerance of 1e-10 applies.
     minres_dense: 25 iterations on a 40x40 random indefinite system where the
     Lanczos vectors lose orthogonality; a 1e-16 perturbation of A already moves
-    x by 2e-5 in the oracle, so only 1e-3 agreement is meaningful there."""
+    x by 2e-5 and the residual history by up to 1.3e-2 in the oracle, so only
+    1e-3 (x) and 5e-2 (history) agreement is meaningful there."""
     import torch
 
     import paper_2205_12721_b200 as P
@@ -191,7 +193,7 @@ def test_minres_matches_reference(name, xtol, its):
     r = P.minres(lambda v: A @ v, g["b"], P.MinresConfig(max_iterations=its, rel_tolerance=1e-10), pre)
     assert r.iterations == int(g["iterations"])
     assert rel(r.x, g["x"]) <= xtol
-    assert np.allclose(r.residual_history, g["history"], rtol=max(xtol, 1e-10), atol=1e-14)
+    assert np.allclose(r.residual_history, g["history"], rtol=htol, atol=1e-14)
 
 
 def test_minres_edge_cases():
