@@ -40,19 +40,20 @@ enum Kind : int {
   K_COUNT = 10
 };
 
-// Tuning knobs (compile-time; see tools/build_variant.sh): threads per CTA,
-// shared-memory budget per CTA in doubles, and the occupancy hint.
+// Tuning knobs (compile-time overrides for tools/build_variant.sh; 0 = the
+// per-order defaults in Cfg): threads per CTA, shared-memory budget per CTA
+// in doubles, and the occupancy hint.
 #ifndef TMOP_ELEM_NT
-#define TMOP_ELEM_NT 256
+#define TMOP_ELEM_NT 0
 #endif
 #ifndef TMOP_SMEM_BUDGET
-#define TMOP_SMEM_BUDGET 14336
+#define TMOP_SMEM_BUDGET 0
 #endif
 #ifndef TMOP_MIN_BLOCKS
-#define TMOP_MIN_BLOCKS 1
+#define TMOP_MIN_BLOCKS 0
 #endif
 constexpr int GRID_CAP = 148 * 8;
-constexpr int ELEM_NT = TMOP_ELEM_NT;
+constexpr int ELEM_NT = 256;   // diagonal kernel
 
 __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -79,8 +80,15 @@ struct Cfg {
   // even number of doubles so every element block is 16-byte aligned (TMA).
   static constexpr int F = DIM * DIM + 2;
   static constexpr int QS = (F * QP + 1) & ~1;
-  // elements per CTA: work arrays + staged Q-data in ~112 KB (2 CTAs / SM)
-  static constexpr int EPB = cclamp(TMOP_SMEM_BUDGET / (PER + QS), 1, 32);
+  // Launch shape, from the A/B sweep of round 1 (profiles/round1_apply_ab.md):
+  // 128-thread CTAs with ~56 KB (4 CTAs / SM) for p = 1, 2, 4; 256-thread
+  // CTAs with ~72 KB (3 CTAs / SM) for p = 3.
+  static constexpr bool WIDE = (DIM == 3 && N == 4);
+  static constexpr int NT = TMOP_ELEM_NT ? TMOP_ELEM_NT : (WIDE ? 256 : 128);
+  static constexpr int MINB = TMOP_MIN_BLOCKS ? TMOP_MIN_BLOCKS : (WIDE ? 3 : 4);
+  static constexpr int BUDGET = TMOP_SMEM_BUDGET ? TMOP_SMEM_BUDGET : (WIDE ? 9216 : 7168);
+  // elements per CTA: work arrays + staged Q-data within BUDGET doubles
+  static constexpr int EPB = cclamp(BUDGET / (PER + QS), 1, 32);
   static constexpr int QOFF = (EPB * PER + 1) & ~1;          // Q-data staging offset (doubles)
   static constexpr int SMEM = EPB * PER * 8;                 // kernels without staging
   static constexpr int SMEM_TMA = (QOFF + EPB * QS) * 8;     // Hessian-action kernels
@@ -113,7 +121,7 @@ template <int DIM, int N, int Q, int C, bool MASK>
 __device__ __forceinline__ void gather(const ElemArgs &a, int64_t e0, double *R1) {
   using CF = Cfg<DIM, N, Q>;
   constexpr int NP = CF::NP, ITEMS = C * NP;
-  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / NP, l = r % NP;
     const int64_t eg = e0 + e;
     double val = 0.0;
@@ -126,13 +134,52 @@ __device__ __forceinline__ void gather(const ElemArgs &a, int64_t e0, double *R1
   }
 }
 
+// Register-prefetching gather (Hessian action): the next group's nodal values
+// are loaded into registers while the current group's transposed sweeps run,
+// and stored to shared memory at the top of the next iteration -- the
+// dependent restriction -> v loads then no longer stall the group start.
+template <int DIM, int N, int Q>
+struct GatherPrefetch {
+  using CF = Cfg<DIM, N, Q>;
+  static constexpr int ITEMS = DIM * CF::NP, TOTAL = CF::EPB * ITEMS;
+  static constexpr int PER_THREAD = (TOTAL + CF::NT - 1) / CF::NT;
+  double val[PER_THREAD];
+  __device__ __forceinline__ void load(const ElemArgs &a, int64_t e0) {
+#pragma unroll
+    for (int j = 0; j < PER_THREAD; ++j) {
+      const int w = threadIdx.x + j * CF::NT;
+      double v = 0.0;
+      if (w < TOTAL) {
+        const int e = w / ITEMS, r = w % ITEMS, c = r / CF::NP, l = r % CF::NP;
+        const int64_t eg = e0 + e;
+        if (eg < a.ne) {
+          const int node = __ldg(a.restr + eg * CF::NP + l);
+          v = __ldg(a.in + c * a.nn + node);
+          if ((__ldg(a.fixed + node) >> c) & 1) v = 0.0;
+        }
+      }
+      val[j] = v;
+    }
+  }
+  __device__ __forceinline__ void store(double *R1) const {
+#pragma unroll
+    for (int j = 0; j < PER_THREAD; ++j) {
+      const int w = threadIdx.x + j * CF::NT;
+      if (w < TOTAL) {
+        const int e = w / ITEMS, r = w % ITEMS;
+        R1[e * CF::R1 + r] = val[j];
+      }
+    }
+  }
+};
+
 // --------------------------------------------------------- 3D forward
 // X[c][kz][ky][kx] (R1) -> U[c][v][qz][ky][kx] (R2), v in {B, G}
 template <int N, int Q, int C>
 __device__ __forceinline__ void f1_3d(const Tab &t, const double *R1, double *R2) {
   using CF = Cfg<3, N, Q>;
   constexpr int ITEMS = C * N * N;
-  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (N * N), kk = r % (N * N);
     const double *x = R1 + e * CF::R1 + c * N * N * N + kk;
     double xv[N];
@@ -158,7 +205,7 @@ template <int N, int Q, int C>
 __device__ __forceinline__ void f2_3d(const Tab &t, const double *R2, double *R1) {
   using CF = Cfg<3, N, Q>;
   constexpr int ITEMS = C * Q * N;
-  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * N), r2 = r % (Q * N), qz = r2 / N, kx = r2 % N;
     const double *ub = R2 + e * CF::R2 + (c * 2 + 0) * Q * N * N + qz * N * N + kx;
     const double *ug = ub + Q * N * N;
@@ -188,7 +235,7 @@ template <int N, int Q, int C>
 __device__ __forceinline__ void f3_3d(const Tab &t, const double *R1, double *R2) {
   using CF = Cfg<3, N, Q>;
   constexpr int ITEMS = C * Q * Q, QP = Q * Q * Q;
-  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * Q), qq = r % (Q * Q);
     constexpr int WF = CF::WF, GF = CF::GF;
     const double *wb = R1 + e * CF::R1 + (c * 3) * WF + qq * CF::NL;
@@ -222,7 +269,7 @@ template <int N, int Q>
 __device__ __forceinline__ void b3_3d(const Tab &t, const double *R2, double *R1) {
   using CF = Cfg<3, N, Q>;
   constexpr int ITEMS = 3 * Q * Q, QP = Q * Q * Q;
-  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * Q), qq = r % (Q * Q);
     constexpr int WF = CF::WF, GF = CF::GF;
     const double *z = R2 + e * CF::R2 + (c * 3) * GF + qq * CF::QL;
@@ -251,7 +298,7 @@ template <int N, int Q>
 __device__ __forceinline__ void b2_3d(const Tab &t, const double *R1, double *R2) {
   using CF = Cfg<3, N, Q>;
   constexpr int ITEMS = 3 * Q * N;
-  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * N), r2 = r % (Q * N), qz = r2 / N, kx = r2 % N;
     constexpr int NL = CF::NL, WF = CF::WF;
     const double *A = R1 + e * CF::R1 + (c * 3) * WF + qz * Q * NL + kx;
@@ -283,7 +330,7 @@ __device__ __forceinline__ void b1_3d(const Tab &t, const double *R2, double *__
                                       int64_t ne) {
   using CF = Cfg<3, N, Q>;
   constexpr int ITEMS = 3 * N * N, NP = N * N * N;
-  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (N * N), kk = r % (N * N);
     if (e0 + e >= ne) continue;
     const double *b = R2 + e * CF::R2 + (c * 2) * Q * N * N + kk;
@@ -307,7 +354,7 @@ template <int N, int Q, int C>
 __device__ __forceinline__ void f1_2d(const Tab &t, const double *R1, double *R2) {
   using CF = Cfg<2, N, Q>;
   constexpr int ITEMS = C * N;
-  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / N, kx = r % N;
     const double *x = R1 + e * CF::R1 + c * N * N + kx;
     double xv[N];
@@ -334,7 +381,7 @@ template <int N, int Q, int C>
 __device__ __forceinline__ void f2_2d(const Tab &t, const double *R2, double *G) {
   using CF = Cfg<2, N, Q>;
   constexpr int ITEMS = C * Q, QP = Q * Q;
-  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / Q, qy = r % Q;
     constexpr int NL = CF::NL, GF = CF::GF;
     const double *ub = R2 + e * CF::R2 + (c * 2) * Q * NL + qy * NL;
@@ -362,7 +409,7 @@ template <int N, int Q>
 __device__ __forceinline__ void b2_2d(const Tab &t, const double *Z, double *R2) {
   using CF = Cfg<2, N, Q>;
   constexpr int ITEMS = 2 * Q, QP = Q * Q;
-  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / Q, qy = r % Q;
     constexpr int NL = CF::NL, GF = CF::GF;
     const double *z = Z + e * CF::R1 + (c * 2) * GF + qy * CF::QL;
@@ -390,7 +437,7 @@ __device__ __forceinline__ void b1_2d(const Tab &t, const double *R2, double *__
                                       int64_t ne) {
   using CF = Cfg<2, N, Q>;
   constexpr int ITEMS = 2 * N, NP = N * N;
-  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += ELEM_NT) {
+  for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / N, kx = r % N;
     if (e0 + e >= ne) continue;
     constexpr int NL = CF::NL;
@@ -458,7 +505,7 @@ __device__ __forceinline__ void lean_hess(int metric, const double *qd, int QP, 
 
 // ------------------------------------------------------ the kernel
 template <int DIM, int N, int Q, int KIND>
-__global__ void __launch_bounds__(ELEM_NT, TMOP_MIN_BLOCKS) elem_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
+__global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
   using CF = Cfg<DIM, N, Q>;
   constexpr int QP = CF::QP, EPB = CF::EPB, QS = CF::QS;
   constexpr bool APPLY = (KIND == K_APPLY || KIND == K_APPLY_NT);
@@ -466,8 +513,8 @@ __global__ void __launch_bounds__(ELEM_NT, TMOP_MIN_BLOCKS) elem_kernel(const El
   double *R1 = smem;
   double *R2 = smem + EPB * CF::R1;
   double *QB = smem + CF::QOFF;   // staged Q-data of the current group (apply only)
-  __shared__ double red_v[ELEM_NT / 32];
-  __shared__ int64_t red_i[ELEM_NT / 32];
+  __shared__ double red_v[CF::NT / 32];
+  __shared__ int64_t red_i[CF::NT / 32];
   __shared__ __align__(8) uint64_t qbar;
 
   double acc = 0.0;
@@ -494,9 +541,18 @@ __global__ void __launch_bounds__(ELEM_NT, TMOP_MIN_BLOCKS) elem_kernel(const El
     if (threadIdx.x == 0 && (int64_t)blockIdx.x < a.ngroups) issue(blockIdx.x);
   }
 
+  GatherPrefetch<DIM, N, Q> pre;
+  if constexpr (APPLY) {
+    if ((int64_t)blockIdx.x < a.ngroups) pre.load(a, (int64_t)blockIdx.x * EPB);
+  }
+
   for (int64_t grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
     const int64_t e0 = grp * EPB;
-    gather<DIM, N, Q, DIM, APPLY>(a, e0, R1);
+    if constexpr (APPLY) {
+      pre.store(R1);
+    } else {
+      gather<DIM, N, Q, DIM, false>(a, e0, R1);
+    }
     __syncthreads();
     // ---- forward: gradients of the gathered field at the points
     double *Gp;
@@ -520,7 +576,7 @@ __global__ void __launch_bounds__(ELEM_NT, TMOP_MIN_BLOCKS) elem_kernel(const El
     __syncthreads();
 
     // ---- point stage
-    for (int w = threadIdx.x; w < EPB * QP; w += ELEM_NT) {
+    for (int w = threadIdx.x; w < EPB * QP; w += CF::NT) {
       const int e = w / QP, q = w % QP;
       const int64_t eg = e0 + e;
       if (eg >= a.ne) continue;
@@ -596,10 +652,11 @@ __global__ void __launch_bounds__(ELEM_NT, TMOP_MIN_BLOCKS) elem_kernel(const El
       phase ^= 1u;
       const int64_t nxt = grp + gridDim.x;
       if (threadIdx.x == 0 && nxt < a.ngroups) issue(nxt);
+      if (nxt < a.ngroups) pre.load(a, nxt * EPB);
     }
 
     if constexpr (KIND == K_ELEMDET) {
-      for (int e = threadIdx.x; e < EPB; e += ELEM_NT) {
+      for (int e = threadIdx.x; e < EPB; e += CF::NT) {
         const int64_t eg = e0 + e;
         if (eg >= a.ne) continue;
         double m = R1[e * CF::R1];
@@ -633,11 +690,11 @@ __global__ void __launch_bounds__(ELEM_NT, TMOP_MIN_BLOCKS) elem_kernel(const El
 
   // ---- per-CTA deterministic partials
   if constexpr (KIND == K_ENERGY || KIND == K_VOLUME) {
-    const double s = block_sum<ELEM_NT>(acc, red_v);
+    const double s = block_sum<CF::NT>(acc, red_v);
     if (threadIdx.x == 0) a.part_sum[blockIdx.x] = s;
   }
   if constexpr (KIND == K_SETUP || KIND == K_GRAD || KIND == K_ENERGY || KIND == K_MINDET) {
-    const MinLoc m = block_minloc<ELEM_NT>(mn, red_v, red_i);
+    const MinLoc m = block_minloc<CF::NT>(mn, red_v, red_i);
     if (threadIdx.x == 0) {
       a.part_min[blockIdx.x] = m.v;
       a.part_arg[blockIdx.x] = m.i;

@@ -15,13 +15,14 @@
 
 namespace tmop {
 
-// TMOP_APPLY_KERNEL=generic selects the work-item kernel for the Hessian
-// action instead of the column kernel (A/B measurements).
+// The work-item kernel (elem_kernel<K_APPLY>) is the default Hessian action;
+// TMOP_APPLY_KERNEL=col selects the column kernel (apply_col_kernel), which
+// measured slower for p >= 2 in round 1 (profiles/round1_apply_ab.md).
 inline bool use_generic_apply() {
   static int v = -1;
   if (v < 0) {
     const char *e = std::getenv("TMOP_APPLY_KERNEL");
-    v = (e && std::strcmp(e, "generic") == 0) ? 1 : 0;
+    v = (e && std::strcmp(e, "col") == 0) ? 0 : 1;
   }
   return v == 1;
 }
@@ -77,7 +78,7 @@ int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
       if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -2;
       configured = true;
     }
-    kfn<<<grid, ELEM_NT, smem, s>>>(a, t);
+    kfn<<<grid, CF::NT, smem, s>>>(a, t);
     return grid;
   }
 }
