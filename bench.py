@@ -215,7 +215,7 @@ def newton_iteration(prob, x):
     t_setup = time.perf_counter() - t
     t = time.perf_counter()
     mr = P.minres(lambda vv: prob.hessian_apply(qd, vv), g,
-                  P.MinresConfig(max_iterations=20, rel_tolerance=1e-300), pre, prob.ctx)
+                  P.MinresConfig(max_iterations=20, rel_tolerance=1e-300), pre, prob.ctx, operator=(prob, qd))
     torch.cuda.synchronize()
     t_minres = time.perf_counter() - t
     t = time.perf_counter()

@@ -181,6 +181,17 @@ int tmop_minres_step(tmop_ctx *ctx, int64_t n, double *Av, const double *r1,
                      const double *w2, double *x, double rtol,
                      tmop_minres_state *st2, int k);
 
+/* One full MINRES iteration for THIS context's Hessian (AddMultGradPA):
+ * Av = H v with the E->L gather fused into the K1 update, then the K2 / K3
+ * kernels of tmop_minres_step -- 4 launches, no host round trip.  Same
+ * buffer rotation contract as tmop_minres_step. */
+int tmop_minres_step_op(tmop_ctx *ctx, const double *qdata, int64_t n,
+                        double *Av, const double *r1, const double *r2,
+                        const double *inv, double *z, double *v,
+                        const double *w, double *w1buf, const double *w2,
+                        double *x, double rtol, tmop_minres_state *st2,
+                        int k);
+
 #ifdef __cplusplus
 }
 #endif

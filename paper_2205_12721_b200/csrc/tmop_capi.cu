@@ -401,4 +401,20 @@ int tmop_minres_step(tmop_ctx *c, int64_t n, double *Av, const double *r1, const
   return TMOP_OK;
 }
 
+int tmop_minres_step_op(tmop_ctx *c, const double *qdata, int64_t n, double *Av, const double *r1, const double *r2,
+                        const double *inv, double *z, double *v, const double *w, double *w1buf, const double *w2,
+                        double *x, double rtol, tmop_minres_state *st2, int k) {
+  if (!c || !qdata || !st2) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (n != c->nn * c->dim) return fail(TMOP_ERR_ARG, "vector length %lld != dim * n_nodes", (long long)n);
+  ElemArgs a = base_args(c);
+  a.in = v;
+  a.qdata = qdata;
+  int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
+  if (rc) return rc;
+  launch_minres_step_op(c->dim, c->nn, c->NP, c->l2e_off, c->l2e_idx, c->E, c->fixed, n, Av, r1, r2, inv, z, v, w,
+                        w1buf, w2, x, rtol, st2 + (k & 1), st2 + ((k + 1) & 1), c->vpart1, c->vpart2, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
 }  // extern "C"

@@ -390,6 +390,62 @@ void launch_minres_init(int64_t n, const double *b, const double *inv, double *x
   minres_init2_kernel<<<g, VEC_NT, 0, s>>>(n, z, v, part, g, st);
 }
 
+// Fused E->L gather + MINRES K1 for the TMOP operator (one pass over Av
+// instead of a gather write followed by a K1 read-modify-write):
+//   Av[i] = (fixed ? v : sum_E) ; Av -= (beta/oldb) r1 (itn >= 2) ; alfa partial v.Av
+// Grid = vec_grid(n), grid-stride over nodes, so the partial array has the
+// same length the following K2 / K3 expect.
+template <int D>
+__global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, int np, const int64_t *__restrict__ off,
+                                                        const uint32_t *__restrict__ idx, const double *__restrict__ E,
+                                                        const uint8_t *__restrict__ fixed, const double *__restrict__ v,
+                                                        const double *__restrict__ r1, double *__restrict__ Av,
+                                                        const tmop_minres_state *cur, double *__restrict__ part) {
+  if (cur->done) return;
+  __shared__ double sv[VEC_NT / 32];
+  const bool sub = cur->itn >= 1;
+  const double f = sub ? cur->beta / cur->oldb : 0.0;
+  double s = 0.0;
+  for (int64_t node = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; node < nn; node += (int64_t)gridDim.x * VEC_NT) {
+    double acc[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) acc[c] = 0.0;
+    for (int64_t k = off[node]; k < off[node + 1]; ++k) {
+      const uint32_t u = __ldg(idx + k);
+      const uint32_t e = u / (uint32_t)np, l = u - e * (uint32_t)np;
+      const double *src = E + (int64_t)e * D * np + l;
+#pragma unroll
+      for (int c = 0; c < D; ++c) acc[c] += __ldg(src + c * np);
+    }
+    const uint8_t fl = __ldg(fixed + node);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const int64_t i = c * nn + node;
+      const double vi = v[i];
+      double y = ((fl >> c) & 1) ? vi : acc[c];
+      if (sub) y = y - f * r1[i];
+      Av[i] = y;
+      s += vi * y;
+    }
+  }
+  s = block_sum<VEC_NT>(s, sv);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+void launch_minres_step_op(int dim, int64_t nn, int np, const int64_t *off, const uint32_t *idx, const double *E,
+                           const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
+                           const double *inv, double *z, double *v, const double *w, double *w1buf, const double *w2,
+                           double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt, double *part1,
+                           double *part2, cudaStream_t s) {
+  const int g = vec_grid(n);
+  if (dim == 2)
+    e2l_minres_k1<2><<<g, VEC_NT, 0, s>>>(nn, np, off, idx, E, fixed, v, r1, Av, cur, part1);
+  else
+    e2l_minres_k1<3><<<g, VEC_NT, 0, s>>>(nn, np, off, idx, E, fixed, v, r1, Av, cur, part1);
+  minres_k2<<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, part2, g);
+  minres_k3<<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol);
+}
+
 void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r2, const double *inv, double *z,
                         double *v, const double *w, double *w1buf, const double *w2, double *x, double rtol,
                         tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, double *part2,

@@ -415,6 +415,9 @@ class TmopProblem:
     def ctx(self):
         return self._ctx
 
+    # newton_solve may run MINRES iterations as single fused library calls
+    supports_fused_minres = True
+
 
 def mesh_volume(mesh: Mesh, rule, coords=None) -> float:
     """Quadrature volume of the mesh image (metrics.py:319-330), on the GPU."""

@@ -164,11 +164,14 @@ _ST = np.dtype([(n, "<f8") for n in ("beta1", "beta", "oldb", "alfa", "beta2", "
                [(n, "<i4") for n in ("itn", "done", "breakdown", "nonpd")])
 
 
-def minres(apply_op: Callable, b, cfg: MinresConfig, precond=None, ctx=None) -> MinresResult:
+def minres(apply_op: Callable, b, cfg: MinresConfig, precond=None, ctx=None, operator=None) -> MinresResult:
     """Preconditioned MINRES from x0 = 0 (solvers.py:93-180), device resident.
 
     `apply_op` maps a device tensor to a device tensor (a numpy result is
-    copied up).  `precond` is a JacobiPreconditioner (or None).
+    copied up).  `precond` is a JacobiPreconditioner (or None).  With
+    `operator=(problem, qdata)` for a device TmopProblem, each iteration is one
+    library call (tmop_minres_step_op: element kernel + E->L gather fused
+    with the first vector update + 2 vector kernels), and apply_op is unused.
     """
     torch = _torch()
     cfg.validate()
@@ -182,8 +185,11 @@ def minres(apply_op: Callable, b, cfg: MinresConfig, precond=None, ctx=None) -> 
         if not isinstance(precond, JacobiPreconditioner):
             raise TypeError("device MINRES takes a JacobiPreconditioner (jacobi_preconditioner(diag))")
         inv = precond.inv
-    bufs = [torch.empty_like(b) for _ in range(8)]
-    x, r1, r2, z, v, w, w1, w2 = bufs
+    bufs = [torch.empty_like(b) for _ in range(9)]
+    x, r1, r2, z, v, w, w1, w2, spare = bufs
+    if operator is not None:
+        op_prob, op_qd = operator
+        ctx = op_prob.ctx
     st = torch.zeros(2 * _lib.MINRES_STATE_BYTES, dtype=torch.uint8, device=dev)
     stp = st.data_ptr()
     _lib.check(lib.tmop_minres_init(ctx, n, _lib.ptr(b), _lib.ptr(inv), _lib.ptr(x), _lib.ptr(r1), _lib.ptr(r2),
@@ -206,6 +212,15 @@ def minres(apply_op: Callable, b, cfg: MinresConfig, precond=None, ctx=None) -> 
     while k < cfg.max_iterations and not done:
         todo = min(cfg.check_every, cfg.max_iterations - k)
         for _ in range(todo):
+            if operator is not None:
+                _lib.check(lib.tmop_minres_step_op(ctx, _lib.ptr(op_qd.data), n, _lib.ptr(spare), _lib.ptr(r1),
+                                                   _lib.ptr(r2), _lib.ptr(inv), _lib.ptr(z), _lib.ptr(v),
+                                                   _lib.ptr(w), _lib.ptr(w1), _lib.ptr(w2), _lib.ptr(x),
+                                                   float(cfg.rel_tolerance), stp, k), "tmop_minres_step_op")
+                r1, r2, spare = r2, spare, r1
+                w1, w2, w = w2, w, w1
+                k += 1
+                continue
             Av = apply_op(v)
             if not type(Av).__module__.startswith("torch"):
                 Av = torch.from_numpy(np.ascontiguousarray(Av, dtype=np.float64)).to(dev)
@@ -373,8 +388,9 @@ def newton_solve(x0, problem: ProblemLike, newton_cfg: NewtonConfig | None = Non
         precond = None
         if minres_cfg.preconditioned:
             precond = jacobi_preconditioner(problem.hessian_diagonal(qdata), ctx)
+        fused = (problem, qdata) if getattr(problem, "supports_fused_minres", False) else None
         try:
-            mr = minres(lambda v: problem.hessian_apply(qdata, v), g, minres_cfg, precond, ctx)
+            mr = minres(lambda v: problem.hessian_apply(qdata, v), g, minres_cfg, precond, ctx, operator=fused)
         except MinresBreakdownError as err:
             return ret(x, trace, False, ng / ng0, ng0, str(err))
         try:

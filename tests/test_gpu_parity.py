@@ -238,3 +238,23 @@ def test_unsupported_configuration_fails_loudly():
     mesh = P.build_box(3, (2, 2, 2), 2)
     with pytest.raises(P._lib.TmopLibraryError if hasattr(P, "_lib") else RuntimeError):
         P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), 12)
+
+
+def test_fused_minres_operator_matches_generic(rng):
+    """tmop_minres_step_op (element kernel + E->L fused with the K1 update)
+    follows the same recurrence as apply_op + tmop_minres_step."""
+    import torch
+
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(3, (6, 5, 4), 2)
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), 4)
+    x = torch.from_numpy(O.perturb(O.box_mesh(3, (6, 5, 4), 2), rng, 0.2)).cuda()
+    qd = p.hessian_setup(x)
+    g = p.gradient(x)
+    pre = P.jacobi_preconditioner(p.hessian_diagonal(qd), p.ctx)
+    cfg = P.MinresConfig(max_iterations=30, rel_tolerance=1e-10)
+    a = P.minres(lambda v: p.hessian_apply(qd, v), g, cfg, pre, p.ctx)
+    b = P.minres(None, g, cfg, pre, p.ctx, operator=(p, qd))
+    assert a.iterations == b.iterations
+    assert float((a.x - b.x).norm() / a.x.norm()) <= 1e-10
+    assert np.allclose(a.residual_history, b.residual_history, rtol=1e-8)
