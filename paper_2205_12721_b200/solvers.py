@@ -32,6 +32,10 @@ class MinresConfig:
     rel_tolerance: float = 1e-8
     preconditioned: bool = True
     check_every: int = 1   # device state is read every k iterations (results identical for any k)
+    # Replay the fused TMOP iteration as a CUDA graph of 6 iterations (the
+    # buffer rotation and the state parity repeat with period 6).  None = auto
+    # (small problems, where launch latency dominates).
+    graph: bool | None = None
 
     def validate(self) -> None:
         if self.max_iterations < 1:
@@ -209,6 +213,55 @@ def minres(apply_op: Callable, b, cfg: MinresConfig, precond=None, ctx=None, ope
     history = [1.0]
     k = 0
     done = False
+    use_graph = operator is not None and (cfg.graph if cfg.graph is not None else n <= 4_000_000)
+    if use_graph and cfg.max_iterations >= 7:
+        # one eager iteration (configures the kernels), then 6-iteration graphs
+        bufs_r = [r1, r2, spare]
+        bufs_w = [w, w1, w2]
+
+        def step(kk):
+            _lib.check(lib.tmop_minres_step_op(ctx, _lib.ptr(op_qd.data), n, _lib.ptr(bufs_r[2]),
+                                               _lib.ptr(bufs_r[0]), _lib.ptr(bufs_r[1]), _lib.ptr(inv), _lib.ptr(z),
+                                               _lib.ptr(v), _lib.ptr(bufs_w[0]), _lib.ptr(bufs_w[1]),
+                                               _lib.ptr(bufs_w[2]), _lib.ptr(x), float(cfg.rel_tolerance), stp, kk),
+                       "tmop_minres_step_op")
+            bufs_r[0], bufs_r[1], bufs_r[2] = bufs_r[1], bufs_r[2], bufs_r[0]
+            bufs_w[1], bufs_w[2], bufs_w[0] = bufs_w[2], bufs_w[0], bufs_w[1]
+
+        step(0)
+        k = 1
+        cur = torch.cuda.current_stream(dev)
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(cur)
+        graph = torch.cuda.CUDAGraph()
+        _lib.check(lib.tmop_ctx_set_stream(ctx, side.cuda_stream), "tmop_ctx_set_stream")
+        try:
+            with torch.cuda.graph(graph, stream=side):
+                for j in range(6):
+                    step(k + j)
+        finally:
+            _lib.check(lib.tmop_ctx_set_stream(ctx, cur.cuda_stream), "tmop_ctx_set_stream")
+        cur.wait_stream(side)
+        s_ = state(k)
+        done = bool(s_["done"])
+        while not done and k + 6 <= cfg.max_iterations:
+            graph.replay()
+            k += 6
+            s_ = state(k)
+            history.append(float(s_["relres"]))
+            done = bool(s_["done"]) or bool(s_["breakdown"])
+        r1, r2, spare = bufs_r
+        w, w1, w2 = bufs_w
+        del graph
+        if s_["breakdown"]:
+            r = b - (apply_op(x).reshape(-1))
+            zz = inv * r if inv is not None else r
+            explicit = np.sqrt(max(float(torch.dot(r, zz).item()), 0.0)) / float(s_["beta1"])
+            history.append(explicit)
+            if explicit <= cfg.rel_tolerance:
+                return MinresResult(x=x.cpu().numpy() if host else x, iterations=int(s_["itn"]),
+                                    rel_residual=explicit, converged=True, residual_history=history)
+            raise MinresBreakdownError(int(s_["itn"]))
     while k < cfg.max_iterations and not done:
         todo = min(cfg.check_every, cfg.max_iterations - k)
         for _ in range(todo):

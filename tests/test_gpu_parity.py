@@ -258,3 +258,21 @@ def test_fused_minres_operator_matches_generic(rng):
     assert a.iterations == b.iterations
     assert float((a.x - b.x).norm() / a.x.norm()) <= 1e-10
     assert np.allclose(a.residual_history, b.residual_history, rtol=1e-8)
+
+
+def test_graph_replayed_minres_matches_eager(rng):
+    import torch
+
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(3, (5, 4, 4), 2)
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), 4)
+    x = torch.from_numpy(O.perturb(O.box_mesh(3, (5, 4, 4), 2), rng, 0.2)).cuda()
+    qd = p.hessian_setup(x)
+    g = p.gradient(x)
+    pre = P.jacobi_preconditioner(p.hessian_diagonal(qd), p.ctx)
+    for its in (50, 17):
+        e = P.minres(None, g, P.MinresConfig(max_iterations=its, graph=False), pre, p.ctx, operator=(p, qd))
+        gr = P.minres(None, g, P.MinresConfig(max_iterations=its, graph=True), pre, p.ctx, operator=(p, qd))
+        assert e.iterations == gr.iterations
+        assert torch.equal(e.x, gr.x)                  # same kernels, same order: bitwise
+        assert e.rel_residual == gr.rel_residual
