@@ -67,7 +67,20 @@ struct Cfg {
   // an odd number of doubles: a half-warp walking consecutive lines then hits
   // 16 distinct bank pairs (even strides caused 2- to 8-way conflicts).
   static constexpr int NL = N | 1;
-  static constexpr int QL = Q | 1;
+  // grad / z x-lines: odd Q unpadded (odd strides are conflict-free); Q a
+  // power of two unpadded but XOR-swizzled (slot x of line l holds point
+  // x ^ ((l / (16/Q)) mod Q)), which keeps both the x-sweep writes (one line per
+  // thread) and the point-stage reads (one point per thread) conflict-free;
+  // other even Q (6) padded to Q + 1.
+  static constexpr bool SWZ = (Q & (Q - 1)) == 0 && Q <= 16;
+  static constexpr int QL = (Q & 1) || SWZ ? Q : Q + 1;
+  __device__ __forceinline__ static int gs(int l, int x) {
+    if constexpr (SWZ) {
+      return l * Q + (x ^ ((l / (16 / Q)) & (Q - 1)));
+    } else {
+      return l * QL + x;
+    }
+  }
   static constexpr int WF = Q * Q * NL;                       // one (c, variant) block of W / A (3D)
   static constexpr int GF = DIM == 3 ? Q * Q * QL : Q * QL;   // one field of grad / z
   // 3D: R1 holds X / W / A (and det scratch); R2 holds U / grad+z / Bv.
@@ -134,31 +147,44 @@ __device__ __forceinline__ void gather(const ElemArgs &a, int64_t e0, double *R1
   }
 }
 
-// Register-prefetching gather (Hessian action): the next group's nodal values
-// are loaded into registers while the current group's transposed sweeps run,
-// and stored to shared memory at the top of the next iteration -- the
-// dependent restriction -> v loads then no longer stall the group start.
+// Register-prefetching gather (Hessian action).  Two stages so no load is
+// consumed right after it is issued: the restriction indices of group g+2
+// and the nodal values of group g+1 are loaded while group g's transposed
+// sweeps run; values are masked and stored to shared memory at the top of
+// the next iteration.
 template <int DIM, int N, int Q>
 struct GatherPrefetch {
   using CF = Cfg<DIM, N, Q>;
   static constexpr int ITEMS = DIM * CF::NP, TOTAL = CF::EPB * ITEMS;
   static constexpr int PER_THREAD = (TOTAL + CF::NT - 1) / CF::NT;
-  double val[PER_THREAD];
-  __device__ __forceinline__ void load(const ElemArgs &a, int64_t e0) {
+  int node[PER_THREAD];       // restriction of the group after next (-1: none)
+  double val[PER_THREAD];     // raw v of the next group
+  uint8_t fl[PER_THREAD];     // fixed flags of the next group
+  __device__ __forceinline__ void load_index(const ElemArgs &a, int64_t e0) {
 #pragma unroll
     for (int j = 0; j < PER_THREAD; ++j) {
       const int w = threadIdx.x + j * CF::NT;
-      double v = 0.0;
+      int nd = -1;
       if (w < TOTAL) {
-        const int e = w / ITEMS, r = w % ITEMS, c = r / CF::NP, l = r % CF::NP;
+        const int e = w / ITEMS, r = w % ITEMS, l = r % CF::NP;
         const int64_t eg = e0 + e;
-        if (eg < a.ne) {
-          const int node = __ldg(a.restr + eg * CF::NP + l);
-          v = __ldg(a.in + c * a.nn + node);
-          if ((__ldg(a.fixed + node) >> c) & 1) v = 0.0;
-        }
+        if (eg < a.ne) nd = __ldg(a.restr + eg * CF::NP + l);
       }
-      val[j] = v;
+      node[j] = nd;
+    }
+  }
+  __device__ __forceinline__ void load_values(const ElemArgs &a) {
+#pragma unroll
+    for (int j = 0; j < PER_THREAD; ++j) {
+      const int w = threadIdx.x + j * CF::NT;
+      const int c = (w % ITEMS) / CF::NP;
+      if (node[j] >= 0) {
+        val[j] = __ldg(a.in + c * a.nn + node[j]);
+        fl[j] = __ldg(a.fixed + node[j]);
+      } else {
+        val[j] = 0.0;
+        fl[j] = 0;
+      }
     }
   }
   __device__ __forceinline__ void store(double *R1) const {
@@ -166,8 +192,8 @@ struct GatherPrefetch {
     for (int j = 0; j < PER_THREAD; ++j) {
       const int w = threadIdx.x + j * CF::NT;
       if (w < TOTAL) {
-        const int e = w / ITEMS, r = w % ITEMS;
-        R1[e * CF::R1 + r] = val[j];
+        const int e = w / ITEMS, r = w % ITEMS, c = r / CF::NP;
+        R1[e * CF::R1 + r] = ((fl[j] >> c) & 1) ? 0.0 : val[j];
       }
     }
   }
@@ -246,7 +272,7 @@ __device__ __forceinline__ void f3_3d(const Tab &t, const double *R1, double *R2
       bg[k] = wb[WF + k];
       gb[k] = wb[2 * WF + k];
     }
-    double *g = R2 + e * CF::R2 + (c * 3) * GF + qq * CF::QL;
+    double *g = R2 + e * CF::R2 + (c * 3) * GF;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -256,9 +282,10 @@ __device__ __forceinline__ void f3_3d(const Tab &t, const double *R1, double *R2
         s1 += tB<Q, N>(t, q, k) * bg[k];
         s2 += tB<Q, N>(t, q, k) * gb[k];
       }
-      g[q] = s0;
-      g[GF + q] = s1;
-      g[2 * GF + q] = s2;
+      const int o = CF::gs(qq, q);
+      g[o] = s0;
+      g[GF + o] = s1;
+      g[2 * GF + o] = s2;
     }
   }
 }
@@ -272,10 +299,15 @@ __device__ __forceinline__ void b3_3d(const Tab &t, const double *R2, double *R1
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * Q), qq = r % (Q * Q);
     constexpr int WF = CF::WF, GF = CF::GF;
-    const double *z = R2 + e * CF::R2 + (c * 3) * GF + qq * CF::QL;
+    const double *z = R2 + e * CF::R2 + (c * 3) * GF;
     double z0[Q], z1[Q], z2[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) { z0[q] = z[q]; z1[q] = z[GF + q]; z2[q] = z[2 * GF + q]; }
+    for (int q = 0; q < Q; ++q) {
+      const int o = CF::gs(qq, q);
+      z0[q] = z[o];
+      z1[q] = z[GF + o];
+      z2[q] = z[2 * GF + o];
+    }
     double *A = R1 + e * CF::R1 + (c * 3) * WF + qq * CF::NL;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -389,7 +421,7 @@ __device__ __forceinline__ void f2_2d(const Tab &t, const double *R2, double *G)
     double vb[N], vg[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) { vb[k] = ub[k]; vg[k] = ug[k]; }
-    double *g = G + e * CF::R1 + (c * 2) * GF + qy * CF::QL;
+    double *g = G + e * CF::R1 + (c * 2) * GF;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       double s0 = 0.0, s1 = 0.0;
@@ -398,8 +430,9 @@ __device__ __forceinline__ void f2_2d(const Tab &t, const double *R2, double *G)
         s0 += tG<Q, N>(t, q, k) * vb[k];
         s1 += tB<Q, N>(t, q, k) * vg[k];
       }
-      g[q] = s0;
-      g[GF + q] = s1;
+      const int o = CF::gs(qy, q);
+      g[o] = s0;
+      g[GF + o] = s1;
     }
   }
 }
@@ -412,10 +445,14 @@ __device__ __forceinline__ void b2_2d(const Tab &t, const double *Z, double *R2)
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / Q, qy = r % Q;
     constexpr int NL = CF::NL, GF = CF::GF;
-    const double *z = Z + e * CF::R1 + (c * 2) * GF + qy * CF::QL;
+    const double *z = Z + e * CF::R1 + (c * 2) * GF;
     double z0[Q], z1[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) { z0[q] = z[q]; z1[q] = z[GF + q]; }
+    for (int q = 0; q < Q; ++q) {
+      const int o = CF::gs(qy, q);
+      z0[q] = z[o];
+      z1[q] = z[GF + o];
+    }
     double *A = R2 + e * CF::R2 + (c * 2) * Q * NL + qy * NL;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -543,7 +580,9 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
 
   GatherPrefetch<DIM, N, Q> pre;
   if constexpr (APPLY) {
-    if ((int64_t)blockIdx.x < a.ngroups) pre.load(a, (int64_t)blockIdx.x * EPB);
+    pre.load_index(a, (int64_t)blockIdx.x * EPB);      // (empty when blockIdx.x >= ngroups)
+    pre.load_values(a);
+    pre.load_index(a, ((int64_t)blockIdx.x + gridDim.x) * EPB);
   }
 
   for (int64_t grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
@@ -580,7 +619,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
       const int e = w / QP, q = w % QP;
       const int64_t eg = e0 + e;
       if (eg >= a.ne) continue;
-      const int gi = (q / Q) * CF::QL + q % Q;   // padded x-line index of the point
+      const int gi = CF::gs(q / Q, q % Q);   // (padded / swizzled) slot of the point
       double *gp = Gp + e * gstride + gi;
       double A[DIM][DIM];
       load_point<DIM>(gp, CF::GF, A);
@@ -652,7 +691,8 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
       phase ^= 1u;
       const int64_t nxt = grp + gridDim.x;
       if (threadIdx.x == 0 && nxt < a.ngroups) issue(nxt);
-      if (nxt < a.ngroups) pre.load(a, nxt * EPB);
+      pre.load_values(a);                              // group nxt (indices loaded last iteration)
+      pre.load_index(a, (nxt + gridDim.x) * EPB);       // group after nxt
     }
 
     if constexpr (KIND == K_ELEMDET) {
@@ -662,7 +702,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
         double m = R1[e * CF::R1];
         int arg = 0;
         for (int q = 1; q < QP; ++q) {
-          const double v = R1[e * CF::R1 + (q / Q) * CF::QL + q % Q];
+          const double v = R1[e * CF::R1 + CF::gs(q / Q, q % Q)];
           if (v < m) { m = v; arg = q; }
         }
         a.elem_min[eg] = m;
