@@ -181,6 +181,11 @@ int tmop_minres_step(tmop_ctx *ctx, int64_t n, double *Av, const double *r1,
                      const double *w2, double *x, double rtol,
                      tmop_minres_state *st2, int k);
 
+/* Optional device array that receives relres after every MINRES iteration
+ * (hist[itn] for itn < capacity) -- the reference's residual_history
+ * (solvers.py:168-176) without host round trips.  NULL disables. */
+int tmop_minres_set_history(tmop_ctx *ctx, double *hist, int capacity);
+
 /* One full MINRES iteration for THIS context's Hessian (AddMultGradPA):
  * Av = H v with the E->L gather fused into the K1 update, then the K2 / K3
  * kernels of tmop_minres_step -- 4 launches, no host round trip.  Same

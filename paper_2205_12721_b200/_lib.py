@@ -67,6 +67,7 @@ _SIGS = {
     "tmop_jacobi_inverse": [_P, _I64, _P, _D, _P, _P],
     "tmop_minres_init": [_P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "tmop_minres_step": [_P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _D, _P, _INT],
+    "tmop_minres_set_history": [_P, _P, _INT],
     "tmop_minres_step_op": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _D, _P, _INT],
     "tmop_last_error": [],
 }

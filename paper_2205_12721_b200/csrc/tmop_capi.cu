@@ -50,6 +50,8 @@ struct tmop_ctx {
   double *part_sum, *part_min;
   int64_t *part_arg;
   double *vpart1, *vpart2;
+  double *hist;      // MINRES residual history (device, optional)
+  int hist_cap;
 };
 
 namespace tmop {
@@ -396,8 +398,15 @@ int tmop_minres_step(tmop_ctx *c, int64_t n, double *Av, const double *r1, const
                      tmop_minres_state *st2, int k) {
   if (!c || !st2) return fail(TMOP_ERR_ARG, "NULL argument");
   launch_minres_step(n, Av, r1, r2, inv, z, v, w, w1buf, w2, x, rtol, st2 + (k & 1), st2 + ((k + 1) & 1), c->vpart1,
-                     c->vpart2, c->stream);
+                     c->vpart2, c->hist, c->hist_cap, c->stream);
   CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_minres_set_history(tmop_ctx *c, double *hist, int capacity) {
+  if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
+  c->hist = hist;
+  c->hist_cap = hist ? capacity : 0;
   return TMOP_OK;
 }
 
@@ -412,7 +421,8 @@ int tmop_minres_step_op(tmop_ctx *c, const double *qdata, int64_t n, double *Av,
   int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
   if (rc) return rc;
   launch_minres_step_op(c->dim, c->nn, c->NP, c->l2e_off, c->l2e_idx, c->E, c->fixed, n, Av, r1, r2, inv, z, v, w,
-                        w1buf, w2, x, rtol, st2 + (k & 1), st2 + ((k + 1) & 1), c->vpart1, c->vpart2, c->stream);
+                        w1buf, w2, x, rtol, st2 + (k & 1), st2 + ((k + 1) & 1), c->vpart1, c->vpart2, c->hist,
+                        c->hist_cap, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }

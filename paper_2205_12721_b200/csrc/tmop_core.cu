@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(VEC_NT) minres_k3(int64_t n, const double *__r
                                                     const double *__restrict__ w2, double *__restrict__ x,
                                                     const tmop_minres_state *cur, tmop_minres_state *nxt,
                                                     const double *__restrict__ part1,
-                                                    const double *__restrict__ part2, int np, double rtol) {
+                                                    const double *__restrict__ part2, int np, double rtol,
+                                                    double *__restrict__ hist, int hist_cap) {
   const tmop_minres_state c = *cur;
   if (c.done) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *nxt = c;
@@ -380,7 +381,10 @@ __global__ void __launch_bounds__(VEC_NT) minres_k3(int64_t n, const double *__r
   } else if (s.relres <= rtol) {
     s.done = 1;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *nxt = s;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *nxt = s;
+    if (hist && s.itn < hist_cap) hist[s.itn] = s.relres;   // residual history (solvers.py:168-176)
+  }
 }
 
 void launch_minres_init(int64_t n, const double *b, const double *inv, double *x, double *r1, double *r2, double *z,
@@ -436,24 +440,24 @@ void launch_minres_step_op(int dim, int64_t nn, int np, const int64_t *off, cons
                            const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
                            const double *inv, double *z, double *v, const double *w, double *w1buf, const double *w2,
                            double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt, double *part1,
-                           double *part2, cudaStream_t s) {
+                           double *part2, double *hist, int hist_cap, cudaStream_t s) {
   const int g = vec_grid(n);
   if (dim == 2)
     e2l_minres_k1<2><<<g, VEC_NT, 0, s>>>(nn, np, off, idx, E, fixed, v, r1, Av, cur, part1);
   else
     e2l_minres_k1<3><<<g, VEC_NT, 0, s>>>(nn, np, off, idx, E, fixed, v, r1, Av, cur, part1);
   minres_k2<<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, part2, g);
-  minres_k3<<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol);
+  minres_k3<<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol, hist, hist_cap);
 }
 
 void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r2, const double *inv, double *z,
                         double *v, const double *w, double *w1buf, const double *w2, double *x, double rtol,
                         tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, double *part2,
-                        cudaStream_t s) {
+                        double *hist, int hist_cap, cudaStream_t s) {
   const int g = vec_grid(n);
   minres_k1<<<g, VEC_NT, 0, s>>>(n, Av, r1, v, cur, part1);
   minres_k2<<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, part2, g);
-  minres_k3<<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol);
+  minres_k3<<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol, hist, hist_cap);
 }
 
 }  // namespace tmop

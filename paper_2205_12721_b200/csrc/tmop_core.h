@@ -27,12 +27,12 @@ void launch_minres_init(int64_t n, const double *b, const double *inv, double *x
 void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r2, const double *inv, double *z,
                         double *v, const double *w, double *w1buf, const double *w2, double *x, double rtol,
                         tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, double *part2,
-                        cudaStream_t s);
+                        double *hist, int hist_cap, cudaStream_t s);
 
 void launch_minres_step_op(int dim, int64_t nn, int np, const int64_t *off, const uint32_t *idx, const double *E,
                            const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
                            const double *inv, double *z, double *v, const double *w, double *w1buf, const double *w2,
                            double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt, double *part1,
-                           double *part2, cudaStream_t s);
+                           double *part2, double *hist, int hist_cap, cudaStream_t s);
 
 }  // namespace tmop

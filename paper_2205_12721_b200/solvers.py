@@ -170,6 +170,18 @@ _ST = np.dtype([(n, "<f8") for n in ("beta1", "beta", "oldb", "alfa", "beta2", "
 
 def minres(apply_op: Callable, b, cfg: MinresConfig, precond=None, ctx=None, operator=None) -> MinresResult:
     """Preconditioned MINRES from x0 = 0 (solvers.py:93-180), device resident.
+    See _minres_body; this wrapper guarantees the library's residual-history
+    pointer never outlives the call."""
+    used = []
+    try:
+        return _minres_body(apply_op, b, cfg, precond, ctx, operator, used)
+    finally:
+        for c in used:
+            _lib.load().tmop_minres_set_history(c, None, 0)
+
+
+def _minres_body(apply_op: Callable, b, cfg: MinresConfig, precond, ctx, operator, used) -> MinresResult:
+    """Preconditioned MINRES from x0 = 0 (solvers.py:93-180), device resident.
 
     `apply_op` maps a device tensor to a device tensor (a numpy result is
     copied up).  `precond` is a JacobiPreconditioner (or None).  With
@@ -196,6 +208,10 @@ def minres(apply_op: Callable, b, cfg: MinresConfig, precond=None, ctx=None, ope
         ctx = op_prob.ctx
     st = torch.zeros(2 * _lib.MINRES_STATE_BYTES, dtype=torch.uint8, device=dev)
     stp = st.data_ptr()
+    hist_dev = torch.full((cfg.max_iterations + 1,), float("nan"), dtype=torch.float64, device=dev)
+    _lib.check(lib.tmop_minres_set_history(ctx, _lib.ptr(hist_dev), cfg.max_iterations + 1),
+               "tmop_minres_set_history")
+    used.append(ctx)
     _lib.check(lib.tmop_minres_init(ctx, n, _lib.ptr(b), _lib.ptr(inv), _lib.ptr(x), _lib.ptr(r1), _lib.ptr(r2),
                                     _lib.ptr(z), _lib.ptr(v), _lib.ptr(w), _lib.ptr(w2), stp), "tmop_minres_init")
 
@@ -211,6 +227,14 @@ def minres(apply_op: Callable, b, cfg: MinresConfig, precond=None, ctx=None, ope
         return MinresResult(x=xr.cpu().numpy() if host else xr, iterations=0, rel_residual=0.0, converged=True,
                             residual_history=[0.0])
     history = [1.0]
+
+    def _history(itn, explicit=None):
+        """[1.0, relres_1, ..., relres_itn] from the device array; at a
+        breakdown the last entry is the explicit residual (solvers.py:161-176)."""
+        h = [1.0] + [float(v) for v in hist_dev[1:itn + 1].cpu().numpy()]
+        if explicit is not None:
+            h[-1] = explicit
+        return h
     k = 0
     done = False
     use_graph = operator is not None and (cfg.graph if cfg.graph is not None else n <= 4_000_000)
@@ -248,7 +272,6 @@ def minres(apply_op: Callable, b, cfg: MinresConfig, precond=None, ctx=None, ope
             graph.replay()
             k += 6
             s_ = state(k)
-            history.append(float(s_["relres"]))
             done = bool(s_["done"]) or bool(s_["breakdown"])
         r1, r2, spare = bufs_r
         w, w1, w2 = bufs_w
@@ -257,10 +280,10 @@ def minres(apply_op: Callable, b, cfg: MinresConfig, precond=None, ctx=None, ope
             r = b - (apply_op(x).reshape(-1))
             zz = inv * r if inv is not None else r
             explicit = np.sqrt(max(float(torch.dot(r, zz).item()), 0.0)) / float(s_["beta1"])
-            history.append(explicit)
             if explicit <= cfg.rel_tolerance:
                 return MinresResult(x=x.cpu().numpy() if host else x, iterations=int(s_["itn"]),
-                                    rel_residual=explicit, converged=True, residual_history=history)
+                                    rel_residual=explicit, converged=True,
+                                    residual_history=_history(int(s_["itn"]), explicit))
             raise MinresBreakdownError(int(s_["itn"]))
     while k < cfg.max_iterations and not done:
         todo = min(cfg.check_every, cfg.max_iterations - k)
@@ -290,26 +313,21 @@ def minres(apply_op: Callable, b, cfg: MinresConfig, precond=None, ctx=None, ope
         if s["nonpd"]:
             raise ValueError("preconditioner is not positive definite")
         its = int(s["itn"])
-        if cfg.check_every == 1 and its == k and not s["breakdown"]:
-            history.append(float(s["relres"]))
         done = bool(s["done"])
         if s["breakdown"]:
             # Krylov space exhausted: decide on an explicit residual (solvers.py:161-172)
             r = b - (apply_op(x).reshape(-1))
             zz = inv * r if inv is not None else r
             explicit = np.sqrt(max(float(torch.dot(r, zz).item()), 0.0)) / float(s["beta1"])
-            history.append(explicit)
             if explicit <= cfg.rel_tolerance:
                 return MinresResult(x=x.cpu().numpy() if host else x, iterations=its, rel_residual=explicit,
-                                    converged=True, residual_history=history)
+                                    converged=True, residual_history=_history(its, explicit))
             raise MinresBreakdownError(its)
     s = state(k)
     its = int(s["itn"])
-    if cfg.check_every != 1:
-        history.append(float(s["relres"]))
     return MinresResult(x=x.cpu().numpy() if host else x, iterations=its, rel_residual=float(s["relres"]),
                         converged=bool(s["done"]) and float(s["relres"]) <= cfg.rel_tolerance,
-                        residual_history=history)
+                        residual_history=_history(its))
 
 
 class ProblemLike(Protocol):
