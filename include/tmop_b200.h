@@ -15,8 +15,11 @@
  *
  * Q-data (the partially assembled Hessian, reference HessQData
  * operator.py:91-138) is stored ELEMENT-BLOCKED and LEAN:
- * qdata[e * stride + field * Q + q], stride = tmop_qdata_stride(ctx) (even,
- * so each element block is 16-byte aligned for TMA bulk copies), fields =
+ * qdata[e * stride + field * Q + slot(q)], stride = tmop_qdata_stride(ctx)
+ * (== 2 mod 16 doubles: every element block is 16-byte aligned for TMA bulk
+ * copies and 8 staged elements map to distinct shared-memory banks); in 3D
+ * slot(q) stores qx as the slowest point index, slot = qy + nq*qz +
+ * nq^2*qx for q = qx + nq*qy + nq^2*qz (2D: slot = q); fields =
  * T (d*d), k0, itau = 1/det T -- d^2 + 2 doubles per point instead of the
  * reference's 4 + 2 d^2.  S = T^{-T} and the four Hessian-template
  * coefficients are recomputed from them;

@@ -1,0 +1,358 @@
+// tmop_apply_xl.cuh -- the 3D Hessian action (AddMultGradPA,
+// operator.py:401-418) in "x-line" form, the default 3D apply kernel.
+//
+// Why this shape (profiles/round1_*.md): on B200 the FP64 pipe is shared by
+// DFMA and DMMA (measured: mixed DFMA+DMMA loops sum to the same ~35 TF/s),
+// so the element contractions stay on DFMA, and the previous work-item
+// kernel was co-limited by shared-memory bandwidth (~6.5 K doubles of
+// shared traffic per p=2 element, 69 % of the LSU wavefront budget) and
+// FP64 issue.  Here one thread owns one x-line (qy, qz) of an element for
+// all three components and keeps, in registers, the x-sweep inputs W, the
+// nine gradient entries of the current point, the point's Hessian action
+// and the transposed x-sweep accumulators A -- the quadrature-point fields
+// (grad, z) never touch shared memory.  The group's lean Q-data arrives by
+// one TMA bulk copy issued a group ahead (the lean record stores qx as the
+// slowest point index, lean_slot(), and the element stride is 2 mod 16
+// doubles, so the X stage reads it conflict-free).  Shared-memory traffic
+// per p=2 element drops from ~6.5 K to ~4 K doubles (incl. the TMA fill).
+//
+// Layout: a CTA owns EPB = 8 elements per group; thread id = e + 8 * item
+// and every shared buffer is element-interleaved (slot * 8 + e), so a
+// half-warp touches two items x eight elements; the padded strides below
+// make every stage's pair of items differ by an odd number of slots, i.e.
+// every 64-bit shared access is conflict-free.
+//
+// Stages per group (z axis first like contract_dofs_to_quad, fe.py:227-239):
+//   F1  item (ky,kx):   gathered z-lines (registers, loaded during the
+//                       previous group's B2 / B1) -> U[c][v][qz][ky][kx], v in {B, G}
+//   F2  item (qz,kx):   U -> W[c][v3][qz][qy][kx], v3 in {BB, BG, GB}
+//   X   item (qy,qz):   W -> grad at the Q points of the line -> lean Hessian
+//                       block (template: _kernels.py:235-258) -> A (x^T sweep)
+//   B2  item (qz,kx):   A -> Bv[c][v][qz][ky][kx]   (y^T sweep, fe.py:242-253)
+//   B1  item (ky,kx):   Bv -> element-interleaved E-vector (z^T sweep)
+// The E-vector is summed to nodes by e2l_kernel (epb = 8 layout) in
+// ascending element order, no atomics.
+#pragma once
+
+#include "tmop_elem.cuh"
+
+namespace tmop {
+
+// Tuning knob (tools/build_variant.sh): occupancy hint (CTAs / SM; 0 = per
+// order default).
+#ifndef TMOP_XL_MINB
+#define TMOP_XL_MINB 0
+#endif
+
+template <int N, int Q>
+struct XlCfg {
+  static constexpr int EPB = 8;
+  static constexpr int NP = N * N * N, QP = Q * Q * Q;
+  static constexpr int LINES = Q * Q;
+  static constexpr int NT = EPB * LINES;
+  // U / Bv: [c][v][qz][ky*N+kx]          (slots; one slot = EPB doubles)
+  static constexpr int U_QZ = N * N;
+  static constexpr int U_SZ = 6 * Q * U_QZ;
+  // W / A:  [c][v3][qz][qy][kx]
+  static constexpr int W_QY = N | 1;
+  static constexpr int W_QZ0 = Q * W_QY;
+  static constexpr int W_QZ = ((N & 1) || (Q & 1)) ? (W_QZ0 | 1) : W_QZ0;
+  static constexpr int W_SZ = 9 * Q * W_QZ;
+  static constexpr int SLOTS = (U_SZ + W_SZ + 1) & ~1;
+  static constexpr int F = 11;                 // lean fields (T, k0, itau)
+  static constexpr int QS = lean_stride(F * QP);
+  static constexpr int QOFF = SLOTS * EPB;     // staged Q-data (doubles), 16-byte aligned
+  static constexpr int SMEM = (QOFF + EPB * QS) * 8;
+  // CTAs / SM: the x-line keeps ~110 doubles live (p = 2: ~250 registers)
+  static constexpr int MINB = TMOP_XL_MINB ? TMOP_XL_MINB : cmax(1, 65536 / ((NT + 31) / 32 * 32 * (N <= 2 ? 168 : 248)));
+};
+
+template <int N, int Q>
+__host__ __device__ constexpr bool xl_supported() {
+  // register / shared-memory budget: p = 1, 2 (the x-line keeps 18 N
+  // doubles of W and A live across the point loop)
+  return N <= 3 && Q <= 6 && Q >= 2;
+}
+
+// Point stage of the x-line: z = (scaled d2mu/dT2) : g from the lean record
+// (T, k0, itau), accumulated straight into the transposed x-sweep:
+// av[c][0][k] += G(qx,k) z[c][0], av[c][v][k] += B(qx,k) z[c][v] (v = 1, 2).
+// Template metrics: S = itau cof(T) is folded into the coefficients and the
+// block (_kernels.py:235-258) is applied with C = cof(T) directly.
+template <int N, bool NTM>
+__device__ __forceinline__ void xl_point(int metric, const double (&qd)[11], const double (&g)[3][3],
+                                         const double (&tg)[N], const double (&tb)[N], double (&av)[3][3][N]) {
+  double T[3][3], C[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) T[i][j] = qd[i * 3 + j];
+  mcof<3>(T, C);
+  auto acc = [&](int c, int n, double z) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) av[c][n][k] += (n == 0 ? tg[k] : tb[k]) * z;
+  };
+  if constexpr (!NTM) {
+    const double k0 = qd[9], itau = qd[10];
+    double c[4];
+    lean_coeffs(metric, k0, itau, mfro2<3>(T), c);
+    const double dt = mdot<3>(T, g);
+    const double ds = itau * mdot<3>(C, g);
+    const double w1 = (c[1] * dt + c[2] * ds) * itau;
+    const double w2 = c[1] * ds;
+    const double c3 = c[3] * (itau * itau);
+    double gs[3][3];
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int n = 0; n < 3; ++n) gs[p][n] = g[0][p] * C[0][n] + g[1][p] * C[1][n] + g[2][p] * C[2][n];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int n = 0; n < 3; ++n) {
+        const double cross = C[a][0] * gs[0][n] + C[a][1] * gs[1][n] + C[a][2] * gs[2][n];
+        acc(a, n, c[0] * g[a][n] + w1 * C[a][n] + w2 * T[a][n] + c3 * cross);
+      }
+  } else {
+    double S[3][3], z[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) S[i][j] = C[i][j] * qd[10];
+    nt_hess<3>(metric, qd[9], S, T, g, z);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int n = 0; n < 3; ++n) acc(a, n, z[a][n]);
+  }
+}
+
+template <int N, int Q, bool NTM>
+__global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::MINB)
+    apply_xl_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
+  using XC = XlCfg<N, Q>;
+  constexpr int EPB = XC::EPB, NP = XC::NP, QP = XC::QP, QS = XC::QS;
+  constexpr int U_QZ = XC::U_QZ, W_QY = XC::W_QY, W_QZ = XC::W_QZ;
+  extern __shared__ __align__(16) double smem[];
+  double *U = smem;                       // U / Bv
+  double *W = smem + XC::U_SZ * EPB;      // W / A
+  double *QB = smem + XC::QOFF;           // the group's lean Q-data (TMA-staged)
+  __shared__ __align__(8) uint64_t qbar;
+
+  const int tid = threadIdx.x;
+  const int e = tid % EPB;                // element slot of this thread (all stages)
+  const int item = tid / EPB;
+
+  // per-stage roles (loop-invariant)
+  const bool r1 = item < N * N;                 // F1 / B1: (ky, kx)
+  const bool r2 = item < Q * N;                 // F2 / B2: (qz, kx)
+  const int i2_kx = item % N, i2_qz = item / N;
+  const int lqy = item % Q, lqz = item / Q;     // X stage: line (qy, qz); all threads
+
+  // shared offsets (doubles) of each stage's item base
+  const int o1 = item * EPB + e;                                     // U[..][qz=0][item]
+  const int o2u = (i2_qz * U_QZ + i2_kx) * EPB + e;                 // U[..][qz][ky=0][kx]
+  const int o2w = (i2_qz * W_QZ + i2_kx) * EPB + e;                 // W[..][qz][qy=0][kx]
+  const int ox = (lqz * W_QZ + lqy * W_QY) * EPB + e;               // W[..][qz][qy][k=0]
+  constexpr int UV = Q * U_QZ * EPB;      // U stride of v (c stride = 2 UV)
+  constexpr int WV = Q * W_QZ * EPB;      // W stride of v3 (c stride = 3 WV)
+
+  // ---- gather prefetch (F1 threads): v z-lines of the next group
+  double xr[3][N];
+  auto gather = [&](int64_t grp) {
+    const int64_t eg = grp * EPB + e;
+    if (r1 && grp < a.ngroups && eg < a.ne) {
+      const int32_t *rr = a.restr + eg * NP + item;
+#pragma unroll
+      for (int kz = 0; kz < N; ++kz) {
+        const int node = __ldg(rr + kz * N * N);
+        const uint8_t f = __ldg(a.fixed + node);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double v = __ldg(a.in + c * a.nn + node);
+          xr[c][kz] = ((f >> c) & 1) ? 0.0 : v;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int kz = 0; kz < N; ++kz) xr[c][kz] = 0.0;
+    }
+  };
+  // ---- lean Q-data: the group's EPB contiguous element records are
+  // streamed into QB by one TMA bulk copy, issued one group ahead (after the
+  // X stage has consumed the previous group's copy).
+  auto issue = [&](int64_t grp) {
+    const int64_t e0 = grp * EPB;
+    const int64_t cnt = (a.ne - e0) < EPB ? (a.ne - e0) : EPB;
+    const uint32_t bytes = (uint32_t)(cnt * QS * 8);
+    mbar_expect_tx(&qbar, bytes);
+    tma_load_1d(QB, a.qdata + e0 * QS, bytes, &qbar);
+  };
+  const double *qb = QB + e * QS + lqy + Q * lqz;   // field 0 of point (qx = 0) of this line
+  auto qload = [&](int qx, double (&qd)[11]) {
+#pragma unroll
+    for (int f = 0; f < 11; ++f) qd[f] = qb[f * QP + Q * Q * qx];
+  };
+  if (tid == 0) {
+    mbar_init(&qbar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0 && (int64_t)blockIdx.x < a.ngroups) issue(blockIdx.x);
+  uint32_t phase = 0;
+
+  gather(blockIdx.x);
+  for (int64_t grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
+    // ---- F1: z-sweep from registers
+    if (r1) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double *u = U + c * 2 * UV + o1;
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          double sb = 0.0, sg = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            sb += tB<Q, N>(t, qz, k) * xr[c][k];
+            sg += tG<Q, N>(t, qz, k) * xr[c][k];
+          }
+          u[qz * U_QZ * EPB] = sb;
+          u[UV + qz * U_QZ * EPB] = sg;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- F2: y-sweep
+    if (r2) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double *ub = U + c * 2 * UV + o2u;
+        double vb[N], vg[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          vb[k] = ub[k * N * EPB];
+          vg[k] = ub[UV + k * N * EPB];
+        }
+        double *w = W + c * 3 * WV + o2w;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            s0 += tB<Q, N>(t, q, k) * vb[k];
+            s1 += tG<Q, N>(t, q, k) * vb[k];
+            s2 += tB<Q, N>(t, q, k) * vg[k];
+          }
+          w[q * W_QY * EPB] = s0;
+          w[WV + q * W_QY * EPB] = s1;
+          w[2 * WV + q * W_QY * EPB] = s2;
+        }
+      }
+    }
+    mbar_wait(&qbar, phase);
+    __syncthreads();
+    // ---- X: x-sweep, point stage, transposed x-sweep, all in registers
+    {
+      double wv[3][3][N], av[3][3][N];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            wv[c][v][k] = W[(c * 3 + v) * WV + ox + k * EPB];
+            av[c][v][k] = 0.0;
+          }
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        double qd[11];
+        qload(qx, qd);
+        double tg[N], tb[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          tg[k] = tG<Q, N>(t, qx, k);
+          tb[k] = tB<Q, N>(t, qx, k);
+        }
+        double g[3][3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            s0 += tg[k] * wv[c][0][k];
+            s1 += tb[k] * wv[c][1][k];
+            s2 += tb[k] * wv[c][2][k];
+          }
+          g[c][0] = s0;
+          g[c][1] = s1;
+          g[c][2] = s2;
+        }
+        xl_point<N, NTM>(a.metric, qd, g, tg, tb, av);
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+#pragma unroll
+          for (int k = 0; k < N; ++k) W[(c * 3 + v) * WV + ox + k * EPB] = av[c][v][k];
+    }
+    gather(grp + gridDim.x);   // next group's z-lines: in flight during B2 / B1
+    __syncthreads();
+    // QB is free again: stream in the next group's Q-data
+    phase ^= 1u;
+    if (tid == 0 && grp + gridDim.x < a.ngroups) issue(grp + gridDim.x);
+    // ---- B2: y^T sweep  A -> Bv (U region)
+    if (r2) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double *A = W + c * 3 * WV + o2w;
+        double a0[Q], a1[Q], a2[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          a0[q] = A[q * W_QY * EPB];
+          a1[q] = A[WV + q * W_QY * EPB];
+          a2[q] = A[2 * WV + q * W_QY * EPB];
+        }
+        double *b = U + c * 2 * UV + o2u;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            s0 += tB<Q, N>(t, q, k) * a0[q] + tG<Q, N>(t, q, k) * a1[q];
+            s1 += tB<Q, N>(t, q, k) * a2[q];
+          }
+          b[k * N * EPB] = s0;
+          b[UV + k * N * EPB] = s1;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- B1: z^T sweep -> element-interleaved E-vector
+    if (r1) {
+      double *out = a.E + (grp * 3 * NP + item) * EPB + e;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double *b = U + c * 2 * UV + o1;
+        double b0[Q], b1[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          b0[q] = b[q * U_QZ * EPB];
+          b1[q] = b[UV + q * U_QZ * EPB];
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < Q; ++q) s += tB<Q, N>(t, q, k) * b0[q] + tG<Q, N>(t, q, k) * b1[q];
+          out[(c * NP + k * N * N) * EPB] = s;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace tmop

@@ -47,6 +47,7 @@ struct tmop_ctx {
   double omega, det_w, inv_s;
   cudaStream_t stream;
   double *E;
+  int e_es;          // E-vector layout written by the last element kernel (e2l_kernel)
   double *part_sum, *part_min;
   int64_t *part_arg;
   double *vpart1, *vpart2;
@@ -98,6 +99,7 @@ static ElemArgs base_args(const tmop_ctx *c) {
   a.coef_g = c->omega * c->det_w * is;
   a.coef_h = c->omega * c->det_w * (is * is);
   a.E = c->E;
+  a.e_es = 0;
   a.part_sum = c->part_sum;
   a.part_min = c->part_min;
   a.part_arg = c->part_arg;
@@ -108,6 +110,7 @@ static int run(tmop_ctx *c, int kind, ElemArgs &a, int *grid_out) {
   const int g = launch_elem(c->dim, c->n1, c->nq, kind, a, c->tab, c->stream);
   if (g < 0) return fail(TMOP_ERR_ARG, "no kernel instance for dim=%d p=%d n_q=%d (kind %d)", c->dim, c->order, c->nq, kind);
   CUDA_TRY(cudaGetLastError());
+  c->e_es = a.e_es;
   if (grid_out) *grid_out = g;
   return TMOP_OK;
 }
@@ -157,7 +160,8 @@ int tmop_ctx_create(tmop_ctx **out, int dim, int order, int n_quad, int64_t n_el
   c->inv_s = inv_scale;
   c->stream = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
-  const size_t esz = (size_t)n_elements * dim * np;
+  // E-vector: element count padded to whole 8-element groups (interleaved layout)
+  const size_t esz = (size_t)((n_elements + 7) / 8 * 8) * dim * np;
   e = cudaMalloc(&c->E, (esz ? esz : 1) * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->part_sum, GRID_CAP * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->part_min, GRID_CAP * sizeof(double));
@@ -205,7 +209,7 @@ int tmop_qdata_fields(const tmop_ctx *c) {
 
 int64_t tmop_qdata_stride(const tmop_ctx *c) {
   if (!c) return -1;
-  return ((int64_t)tmop_qdata_fields(c) * c->QP + 1) & ~(int64_t)1;
+  return lean_stride(tmop_qdata_fields(c) * c->QP);
 }
 
 int64_t tmop_qdata_size(const tmop_ctx *c) {
@@ -226,9 +230,9 @@ int tmop_qdata_to_reference(tmop_ctx *c, const double *qdata, double *out) {
   const unsigned grid = (unsigned)((nq + nt - 1) / nt);
   const int qs = (int)tmop_qdata_stride(c);
   if (c->dim == 2)
-    qdata_expand_kernel<2><<<grid, nt, 0, c->stream>>>(c->metric, c->ne, c->QP, qs, qdata, out);
+    qdata_expand_kernel<2><<<grid, nt, 0, c->stream>>>(c->metric, c->ne, c->nq, c->QP, qs, qdata, out);
   else
-    qdata_expand_kernel<3><<<grid, nt, 0, c->stream>>>(c->metric, c->ne, c->QP, qs, qdata, out);
+    qdata_expand_kernel<3><<<grid, nt, 0, c->stream>>>(c->metric, c->ne, c->nq, c->QP, qs, qdata, out);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }
@@ -258,7 +262,7 @@ int tmop_hessian_apply(tmop_ctx *c, const double *qdata, const double *v, double
   a.qdata = qdata;
   int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
   if (rc) return rc;
-  launch_e2l(c->dim, c->nn, c->NP, c->l2e_off, c->l2e_idx, c->E, c->fixed, 0, v, nullptr, y, c->stream);
+  launch_e2l(c->dim, c->nn, c->NP, c->e_es, c->l2e_off, c->l2e_idx, c->E, c->fixed, 0, v, nullptr, y, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }
@@ -273,7 +277,7 @@ int tmop_hessian_apply_elements(tmop_ctx *c, const double *qdata, const double *
 
 int tmop_hessian_apply_gather(tmop_ctx *c, const double *v, double *y) {
   if (!c || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
-  launch_e2l(c->dim, c->nn, c->NP, c->l2e_off, c->l2e_idx, c->E, c->fixed, 0, v, nullptr, y, c->stream);
+  launch_e2l(c->dim, c->nn, c->NP, c->e_es, c->l2e_off, c->l2e_idx, c->E, c->fixed, 0, v, nullptr, y, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }
@@ -284,7 +288,7 @@ int tmop_hessian_diagonal(tmop_ctx *c, const double *qdata, double *diag) {
   a.qdata = qdata;
   int rc = run(c, metric_is_template(c->metric) ? K_DIAG : K_DIAG_NT, a, nullptr);
   if (rc) return rc;
-  launch_e2l(c->dim, c->nn, c->NP, c->l2e_off, c->l2e_idx, c->E, c->fixed, 2, nullptr, nullptr, diag, c->stream);
+  launch_e2l(c->dim, c->nn, c->NP, c->e_es, c->l2e_off, c->l2e_idx, c->E, c->fixed, 2, nullptr, nullptr, diag, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }
@@ -296,7 +300,7 @@ int tmop_gradient(tmop_ctx *c, const double *x, double *grad, tmop_det_status *d
   int g = 0;
   int rc = run(c, K_GRAD, a, &g);
   if (rc) return rc;
-  launch_e2l(c->dim, c->nn, c->NP, c->l2e_off, c->l2e_idx, c->E, c->fixed, 1, nullptr, nullptr, grad, c->stream);
+  launch_e2l(c->dim, c->nn, c->NP, c->e_es, c->l2e_off, c->l2e_idx, c->E, c->fixed, 1, nullptr, nullptr, grad, c->stream);
   launch_fin(g, nullptr, c->part_min, c->part_arg, 0.0, nullptr, 0.0, nullptr, det_out, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
@@ -420,7 +424,7 @@ int tmop_minres_step_op(tmop_ctx *c, const double *qdata, int64_t n, double *Av,
   a.qdata = qdata;
   int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
   if (rc) return rc;
-  launch_minres_step_op(c->dim, c->nn, c->NP, c->l2e_off, c->l2e_idx, c->E, c->fixed, n, Av, r1, r2, inv, z, v, w,
+  launch_minres_step_op(c->dim, c->nn, c->NP, c->e_es, c->l2e_off, c->l2e_idx, c->E, c->fixed, n, Av, r1, r2, inv, z, v, w,
                         w1buf, w2, x, rtol, st2 + (k & 1), st2 + ((k + 1) & 1), c->vpart1, c->vpart2, c->hist,
                         c->hist_cap, c->stream);
   CUDA_TRY(cudaGetLastError());

@@ -17,8 +17,17 @@ namespace tmop {
 // copy v, operator.py:417), 1 = gradient (constrained -> 0, operator.py:345),
 // 2 = diagonal (constrained -> 1, operator.py:458).  `add` (may be NULL) is
 // an extra T-vector added before the constraint fix-up (limiting term).
+// E layout: element groups of 2^es elements interleaved (element fastest):
+// E[((e >> es) * D * np + c * np + l) << es | (e & (2^es - 1))]; es = 0 is
+// the plain element-blocked layout E[e][c][l].
+__device__ __forceinline__ const double *e_src(const double *E, uint32_t u, int np, int D, int es, int64_t &cs) {
+  const uint32_t e = u / (uint32_t)np, l = u - e * (uint32_t)np;
+  cs = (int64_t)np << es;
+  return E + ((((int64_t)(e >> es) * D * np + l) << es) | (int64_t)(e & ((1u << es) - 1u)));
+}
+
 template <int D>
-__global__ void e2l_kernel(int64_t nn, int np, const int64_t *__restrict__ off, const uint32_t *__restrict__ idx,
+__global__ void e2l_kernel(int64_t nn, int np, int es, const int64_t *__restrict__ off, const uint32_t *__restrict__ idx,
                            const double *__restrict__ E, const uint8_t *__restrict__ fixed, int mode,
                            const double *__restrict__ v, const double *__restrict__ add, double *__restrict__ y) {
   const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -28,11 +37,10 @@ __global__ void e2l_kernel(int64_t nn, int np, const int64_t *__restrict__ off, 
 #pragma unroll
   for (int c = 0; c < D; ++c) acc[c] = 0.0;
   for (int64_t k = b; k < end; ++k) {
-    const uint32_t u = __ldg(idx + k);
-    const uint32_t e = u / (uint32_t)np, l = u - e * (uint32_t)np;
-    const double *src = E + (int64_t)e * D * np + l;
+    int64_t cs;
+    const double *src = e_src(E, __ldg(idx + k), np, D, es, cs);
 #pragma unroll
-    for (int c = 0; c < D; ++c) acc[c] += __ldg(src + c * np);
+    for (int c = 0; c < D; ++c) acc[c] += __ldg(src + c * cs);
   }
   const uint8_t f = __ldg(fixed + node);
 #pragma unroll
@@ -45,15 +53,15 @@ __global__ void e2l_kernel(int64_t nn, int np, const int64_t *__restrict__ off, 
   }
 }
 
-int launch_e2l(int dim, int64_t nn, int np, const int64_t *off, const uint32_t *idx, const double *E,
+int launch_e2l(int dim, int64_t nn, int np, int es, const int64_t *off, const uint32_t *idx, const double *E,
                const uint8_t *fixed, int mode, const double *v, const double *add, double *y, cudaStream_t s) {
   const int nt = 256;
   const int64_t grid = (nn + nt - 1) / nt;
   if (grid == 0) return 0;
   if (dim == 2)
-    e2l_kernel<2><<<(unsigned)grid, nt, 0, s>>>(nn, np, off, idx, E, fixed, mode, v, add, y);
+    e2l_kernel<2><<<(unsigned)grid, nt, 0, s>>>(nn, np, es, off, idx, E, fixed, mode, v, add, y);
   else
-    e2l_kernel<3><<<(unsigned)grid, nt, 0, s>>>(nn, np, off, idx, E, fixed, mode, v, add, y);
+    e2l_kernel<3><<<(unsigned)grid, nt, 0, s>>>(nn, np, es, off, idx, E, fixed, mode, v, add, y);
   return 0;
 }
 
@@ -400,7 +408,7 @@ void launch_minres_init(int64_t n, const double *b, const double *inv, double *x
 // Grid = vec_grid(n), grid-stride over nodes, so the partial array has the
 // same length the following K2 / K3 expect.
 template <int D>
-__global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, int np, const int64_t *__restrict__ off,
+__global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, int np, int es, const int64_t *__restrict__ off,
                                                         const uint32_t *__restrict__ idx, const double *__restrict__ E,
                                                         const uint8_t *__restrict__ fixed, const double *__restrict__ v,
                                                         const double *__restrict__ r1, double *__restrict__ Av,
@@ -415,11 +423,10 @@ __global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, int np, cons
 #pragma unroll
     for (int c = 0; c < D; ++c) acc[c] = 0.0;
     for (int64_t k = off[node]; k < off[node + 1]; ++k) {
-      const uint32_t u = __ldg(idx + k);
-      const uint32_t e = u / (uint32_t)np, l = u - e * (uint32_t)np;
-      const double *src = E + (int64_t)e * D * np + l;
+      int64_t cs;
+      const double *src = e_src(E, __ldg(idx + k), np, D, es, cs);
 #pragma unroll
-      for (int c = 0; c < D; ++c) acc[c] += __ldg(src + c * np);
+      for (int c = 0; c < D; ++c) acc[c] += __ldg(src + c * cs);
     }
     const uint8_t fl = __ldg(fixed + node);
 #pragma unroll
@@ -436,16 +443,16 @@ __global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, int np, cons
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-void launch_minres_step_op(int dim, int64_t nn, int np, const int64_t *off, const uint32_t *idx, const double *E,
+void launch_minres_step_op(int dim, int64_t nn, int np, int es, const int64_t *off, const uint32_t *idx, const double *E,
                            const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
                            const double *inv, double *z, double *v, const double *w, double *w1buf, const double *w2,
                            double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt, double *part1,
                            double *part2, double *hist, int hist_cap, cudaStream_t s) {
   const int g = vec_grid(n);
   if (dim == 2)
-    e2l_minres_k1<2><<<g, VEC_NT, 0, s>>>(nn, np, off, idx, E, fixed, v, r1, Av, cur, part1);
+    e2l_minres_k1<2><<<g, VEC_NT, 0, s>>>(nn, np, es, off, idx, E, fixed, v, r1, Av, cur, part1);
   else
-    e2l_minres_k1<3><<<g, VEC_NT, 0, s>>>(nn, np, off, idx, E, fixed, v, r1, Av, cur, part1);
+    e2l_minres_k1<3><<<g, VEC_NT, 0, s>>>(nn, np, es, off, idx, E, fixed, v, r1, Av, cur, part1);
   minres_k2<<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, part2, g);
   minres_k3<<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol, hist, hist_cap);
 }

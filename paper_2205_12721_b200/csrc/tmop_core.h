@@ -13,7 +13,7 @@ constexpr int VEC_NT = 256;
 constexpr int VEC_GRID_CAP = 148 * 4;
 
 int vec_grid(int64_t n);
-int launch_e2l(int dim, int64_t nn, int np, const int64_t *off, const uint32_t *idx, const double *E,
+int launch_e2l(int dim, int64_t nn, int np, int es, const int64_t *off, const uint32_t *idx, const double *E,
                const uint8_t *fixed, int mode, const double *v, const double *add, double *y, cudaStream_t s);
 void launch_fin(int nparts, const double *psum, const double *pmin, const int64_t *parg, double sum_scale,
                 double *sum_out, double add_scale, const double *add, tmop_det_status *det_out, cudaStream_t s);
@@ -29,7 +29,7 @@ void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r
                         tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, double *part2,
                         double *hist, int hist_cap, cudaStream_t s);
 
-void launch_minres_step_op(int dim, int64_t nn, int np, const int64_t *off, const uint32_t *idx, const double *E,
+void launch_minres_step_op(int dim, int64_t nn, int np, int es, const int64_t *off, const uint32_t *idx, const double *E,
                            const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
                            const double *inv, double *z, double *v, const double *w, double *w1buf, const double *w2,
                            double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt, double *part1,

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(ELEM_NT) diag2_kernel(const ElemArgs a, const 
         continue;
       }
       double T[DIM][DIM], S[DIM][DIM], k0, itau;
-      lean_load<DIM>(a.qdata + eg * QS + q, QP, T, S, k0, itau);
+      lean_load<DIM>(a.qdata + eg * QS + lean_slot<DIM, Q>(q), QP, T, S, k0, itau);
       if constexpr (!NTM) {
         double c[4];
         lean_coeffs(a.metric, k0, itau, mfro2<DIM>(T), c);

@@ -59,6 +59,13 @@ __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * i
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int cclamp(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// Element stride of the lean Q-data record (doubles): the smallest value
+// >= fields * points with stride == 2 (mod 16).  Even, so every element
+// block is 16-byte aligned (TMA bulk copies), and == 2 (mod 16) so that 8
+// element-interleaved threads reading the same field/slot of 8 consecutive
+// staged elements hit 8 distinct bank pairs (apply_xl_kernel).
+__host__ __device__ constexpr int lean_stride(int n) { return n + ((18 - n % 16) % 16); }
+
 template <int DIM, int N, int Q>
 struct Cfg {
   static constexpr int NP = ipow(N, DIM);
@@ -92,7 +99,7 @@ struct Cfg {
   // lean Q-data: T (d*d), k0, itau per point; element stride rounded to an
   // even number of doubles so every element block is 16-byte aligned (TMA).
   static constexpr int F = DIM * DIM + 2;
-  static constexpr int QS = (F * QP + 1) & ~1;
+  static constexpr int QS = lean_stride(F * QP);
   // Launch shape, from the A/B sweep of round 1 (profiles/round1_apply_ab.md):
   // 128-thread CTAs with ~56 KB (4 CTAs / SM) for p = 1, 2, 4; 256-thread
   // CTAs with ~72 KB (3 CTAs / SM) for p = 3.
@@ -109,6 +116,7 @@ struct Cfg {
 
 struct ElemArgs {
   int64_t ne, nn, ngroups;
+  int e_es;                           // out: log2 of the E-vector element interleave (e2l_kernel)
   const int32_t *__restrict__ restr;
   const uint8_t *__restrict__ fixed;
   const double *__restrict__ in;      // x (positions) or v (direction), T-vector
@@ -128,6 +136,19 @@ struct ElemArgs {
   double coef_g;      // omega * det_w * inv_s       (operator.py:330)
   double coef_h;      // omega * det_w * inv_s^2     (operator.py:358-359)
 };
+
+// Point slot of quadrature point q (x fastest, fe.py:134-140) inside a lean
+// Q-data field: 3D records store qx as the SLOWEST index (slot = line +
+// Q^2 qx, line = qy + Q qz), so the x-line kernel's threads (one per line)
+// read each field of one point with unit stride.  2D: identity.
+template <int DIM, int Q>
+__host__ __device__ __forceinline__ int lean_slot(int q) {
+  if constexpr (DIM == 3) {
+    return q / Q + Q * Q * (q % Q);
+  } else {
+    return q;
+  }
+}
 
 // ------------------------------------------------------------- gather
 template <int DIM, int N, int Q, int C, bool MASK>
@@ -626,7 +647,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
 
       if constexpr (APPLY) {
         double z[DIM][DIM];
-        lean_hess<DIM, KIND == K_APPLY_NT>(a.metric, QB + e * QS + q, QP, A, z);
+        lean_hess<DIM, KIND == K_APPLY_NT>(a.metric, QB + e * QS + lean_slot<DIM, Q>(q), QP, A, z);
         store_point<DIM>(gp, CF::GF, z);
       } else {
         // A is the Jacobian dx/dxi at the point
@@ -657,7 +678,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
             acc += wpt * metric_mu<DIM>(a.metric, tau, I1, S);
           } else if constexpr (KIND == K_SETUP) {
             // lean record (operator.py:350-371 restated; see lean_k0)
-            double *qo = a.qout + eg * QS + q;
+            double *qo = a.qout + eg * QS + lean_slot<DIM, Q>(q);
             store_point<DIM>(qo, QP, T);
             qo[DIM * DIM * QP] = lean_k0(a.metric, a.coef_h * wpt, tau);
             qo[(DIM * DIM + 1) * QP] = 1.0 / tau;
@@ -747,7 +768,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
 // from the lean record: template metrics -> coeffs (4), S, T; non-template
 // -> w (1), S, T.  out is (fields_ref, ne * QP) planar.
 template <int D>
-__global__ void qdata_expand_kernel(int metric, int64_t ne, int QP, int QS, const double *__restrict__ qd,
+__global__ void qdata_expand_kernel(int metric, int64_t ne, int q1d, int QP, int QS, const double *__restrict__ qd,
                                     double *__restrict__ out) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nq = ne * QP;
@@ -755,7 +776,8 @@ __global__ void qdata_expand_kernel(int metric, int64_t ne, int QP, int QS, cons
   const int64_t e = k / QP;
   const int q = (int)(k - e * QP);
   double T[D][D], S[D][D], k0, itau;
-  lean_load<D>(qd + e * QS + q, QP, T, S, k0, itau);
+  const int slot = D == 3 ? q / q1d + q1d * q1d * (q % q1d) : q;   // lean_slot
+  lean_load<D>(qd + e * QS + slot, QP, T, S, k0, itau);
   int f = 0;
   if (metric_is_template(metric)) {
     double c[4];

@@ -8,38 +8,46 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "tmop_apply_col.cuh"
+#include "tmop_apply_xl.cuh"
 #include "tmop_diag.cuh"
 #include "tmop_elem.cuh"
 #include "tmop_internal.h"
 
 namespace tmop {
 
-// The work-item kernel (elem_kernel<K_APPLY>) is the default Hessian action;
-// TMOP_APPLY_KERNEL=col selects the column kernel (apply_col_kernel), which
-// measured slower for p >= 2 in round 1 (profiles/round1_apply_ab.md).
-inline bool use_generic_apply() {
+// TMOP_APPLY_KERNEL=generic forces the work-item kernel (A/B and parity).
+inline bool force_generic_apply() {
   static int v = -1;
   if (v < 0) {
     const char *e = std::getenv("TMOP_APPLY_KERNEL");
-    v = (e && std::strcmp(e, "col") == 0) ? 0 : 1;
+    v = (e && std::strcmp(e, "generic") == 0) ? 1 : 0;
   }
   return v == 1;
 }
 
+// 3D Hessian action: the x-line kernel (apply_xl_kernel) where instantiated
+// (p <= 2), else the work-item kernel (elem_kernel<K_APPLY>).  The grid is
+// one persistent wave: 148 SMs x the occupancy the kernel achieves.
 template <int N, int Q, bool NTM>
-int launch_col(ElemArgs &a, const Tab &t, cudaStream_t s) {
-  using CC = ColCfg<N, Q>;
-  a.ngroups = (a.ne + CC::E - 1) / CC::E;
-  const int grid = (int)std::min<int64_t>(a.ngroups, GRID_CAP);
-  if (grid == 0) return 0;
-  auto kfn = apply_col_kernel<N, Q, NTM>;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM) != cudaSuccess) return -2;
-    configured = true;
+int launch_xl(ElemArgs &a, const Tab &t, cudaStream_t s) {
+  using XC = XlCfg<N, Q>;
+  a.ngroups = (a.ne + XC::EPB - 1) / XC::EPB;
+  a.e_es = 3;
+  static_assert(XC::EPB == 8, "e_es assumes 8-element groups");
+  auto kfn = apply_xl_kernel<N, Q, NTM>;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, XC::SMEM) != cudaSuccess) return -2;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, XC::NT, XC::SMEM) != cudaSuccess || nb < 1) nb = 1;
+    per_sm = nb;
   }
-  kfn<<<grid, CC::NT, CC::SMEM, s>>>(a, t);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>(a.ngroups, (int64_t)sms * per_sm);
+  if (grid == 0) return 0;
+  kfn<<<grid, XC::NT, XC::SMEM, s>>>(a, t);
   return grid;
 }
 
@@ -65,8 +73,8 @@ int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
   if constexpr (KIND == K_DIAG || KIND == K_DIAG_NT) {
     return launch_diag<DIM, N, Q, KIND == K_DIAG_NT>(a, t, s);
   } else {
-    if constexpr (DIM == 3 && (KIND == K_APPLY || KIND == K_APPLY_NT) && col_supported<N, Q>()) {
-      if (!use_generic_apply()) return launch_col<N, Q, KIND == K_APPLY_NT>(a, t, s);
+    if constexpr (DIM == 3 && (KIND == K_APPLY || KIND == K_APPLY_NT) && xl_supported<N, Q>()) {
+      if (!force_generic_apply()) return launch_xl<N, Q, KIND == K_APPLY_NT>(a, t, s);
     }
     a.ngroups = (a.ne + CF::EPB - 1) / CF::EPB;
     const int grid = (int)std::min<int64_t>(a.ngroups, GRID_CAP);

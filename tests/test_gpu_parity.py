@@ -59,10 +59,11 @@ def test_storage_accounting_and_blocks():
     p = make(g)
     qd = p.hessian_setup(g["x"])
     # lean format: T (9) + k0 + itau per point; the reference stores 22
-    # (test_operator.py:133-138) -- same information, half the bytes
+    # (test_operator.py:133-138) -- same information, half the bytes.  The
+    # element stride is padded to 2 (mod 16) doubles (704 -> 706).
     assert qd.reference_nbytes == 22 * 64 * 8 * 8
-    assert qd.nbytes == 11 * 64 * 8 * 8
-    assert qd.bytes_per_element == 11 * 64 * 8
+    assert qd.nbytes == 706 * 8 * 8
+    assert qd.bytes_per_element == 706 * 8
     from oracle.tmop_oracle import metric_second
     T = g["t_mat"][:, :, 13]
     want = metric_second(303, T) * g["wq"][13]
