@@ -61,8 +61,12 @@ struct XlCfg {
   static constexpr int SLOTS = (U_SZ + W_SZ + 1) & ~1;
   static constexpr int F = 11;                 // lean fields (T, k0, itau)
   static constexpr int QS = lean_stride(F * QP);
-  static constexpr int QOFF = SLOTS * EPB;     // staged Q-data (doubles), 16-byte aligned
+  static constexpr int XOFF = SLOTS * EPB;                 // gathered v: XS[c][l][e]
+  static constexpr int FOFF = XOFF + 3 * NP * EPB;         // fixed-flag words: FS[l][e] (uint32)
+  static constexpr int BOFF = FOFF + (NP * EPB + 1) / 2;   // flag byte offsets: FB[l][e] (uint8)
+  static constexpr int QOFF = (BOFF + (NP * EPB + 7) / 8 + 1) & ~1;   // staged Q-data, 16-byte aligned
   static constexpr int SMEM = (QOFF + EPB * QS) * 8;
+  static constexpr int GJ = (EPB * NP + NT - 1) / NT;      // gather (element, node) pairs per thread
   // CTAs / SM: the x-line keeps ~110 doubles live (p = 2: ~250 registers)
   static constexpr int MINB = TMOP_XL_MINB ? TMOP_XL_MINB : cmax(1, 65536 / ((NT + 31) / 32 * 32 * (N <= 2 ? 168 : 248)));
 };
@@ -70,8 +74,9 @@ struct XlCfg {
 template <int N, int Q>
 __host__ __device__ constexpr bool xl_supported() {
   // register / shared-memory budget: p = 1, 2 (the x-line keeps 18 N
-  // doubles of W and A live across the point loop)
-  return N <= 3 && Q <= 6 && Q >= 2;
+  // doubles of W and A live across the point loop) and the CTA's work
+  // buffers + staged Q-data within 227 KB
+  return N <= 3 && Q >= 2 && XlCfg<N, Q>::SMEM <= 227 * 1024;
 }
 
 // Point stage of the x-line: z = (scaled d2mu/dT2) : g from the lean record
@@ -127,6 +132,16 @@ __device__ __forceinline__ void xl_point(int metric, const double (&qd)[11], con
   }
 }
 
+// cp.async (LDGSTS): global -> shared without register staging.
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int N, int Q, bool NTM>
 __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::MINB)
     apply_xl_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
@@ -157,28 +172,39 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::MINB)
   constexpr int UV = Q * U_QZ * EPB;      // U stride of v (c stride = 2 UV)
   constexpr int WV = Q * W_QZ * EPB;      // W stride of v3 (c stride = 3 WV)
 
-  // ---- gather prefetch (F1 threads): v z-lines of the next group
-  double xr[3][N];
-  auto gather = [&](int64_t grp) {
-    const int64_t eg = grp * EPB + e;
-    if (r1 && grp < a.ngroups && eg < a.ne) {
-      const int32_t *rr = a.restr + eg * NP + item;
+  // ---- gather: asynchronous.  Every thread owns GJ (element, local node)
+  // pairs of a group (element-fastest, matching the interleaved buffers);
+  // the restriction indices of group g + 2 are loaded during group g, and
+  // once F1 has consumed the gather buffer, cp.async copies v[c][node] and
+  // the 4-byte word holding fixed[node] of group g + 1 straight into shared
+  // memory, landing during F2 / X / B2 / B1.  F1 applies the constraint mask
+  // (operator.py:409).
+  double *XS = smem + XC::XOFF;
+  uint32_t *FS = reinterpret_cast<uint32_t *>(smem + XC::FOFF);
+  uint8_t *FB = reinterpret_cast<uint8_t *>(smem + XC::BOFF);
+  int nd[XC::GJ];
+  auto load_index = [&](int64_t grp) {
 #pragma unroll
-      for (int kz = 0; kz < N; ++kz) {
-        const int node = __ldg(rr + kz * N * N);
-        const uint8_t f = __ldg(a.fixed + node);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double v = __ldg(a.in + c * a.nn + node);
-          xr[c][kz] = ((f >> c) & 1) ? 0.0 : v;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int kz = 0; kz < N; ++kz) xr[c][kz] = 0.0;
+    for (int j = 0; j < XC::GJ; ++j) {
+      const int w = tid + j * XC::NT;
+      const int64_t eg = grp * EPB + w % EPB;
+      nd[j] = (w < EPB * NP && grp < a.ngroups && eg < a.ne) ? __ldg(a.restr + eg * NP + w / EPB) : -1;
     }
+  };
+  auto issue_gather = [&]() {
+#pragma unroll
+    for (int j = 0; j < XC::GJ; ++j) {
+      const int w = tid + j * XC::NT;
+      if (nd[j] >= 0) {
+        const int ge = w % EPB, l = w / EPB;
+        const int64_t node = nd[j];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cp_async8(XS + (c * NP + l) * EPB + ge, a.in + c * a.nn + node);
+        cp_async4(FS + l * EPB + ge, reinterpret_cast<const uint32_t *>(a.fixed + (node & ~(int64_t)3)));
+        FB[l * EPB + ge] = (uint8_t)(8 * (node & 3));
+      }
+    }
+    cp_async_commit();
   };
   // ---- lean Q-data: the group's EPB contiguous element records are
   // streamed into QB by one TMA bulk copy, issued one group ahead (after the
@@ -203,10 +229,22 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::MINB)
   if (tid == 0 && (int64_t)blockIdx.x < a.ngroups) issue(blockIdx.x);
   uint32_t phase = 0;
 
-  gather(blockIdx.x);
+  load_index(blockIdx.x);
+  issue_gather();
+  load_index((int64_t)blockIdx.x + gridDim.x);
   for (int64_t grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
-    // ---- F1: z-sweep from registers
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- F1: z-sweep of the gathered z-lines (masked)
     if (r1) {
+      double xv[3][N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const int l = k * N * N + item;
+        const uint32_t fw = FS[l * EPB + e] >> FB[l * EPB + e];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) xv[c][k] = ((fw >> c) & 1u) ? 0.0 : XS[(c * NP + l) * EPB + e];
+      }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         double *u = U + c * 2 * UV + o1;
@@ -215,8 +253,8 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::MINB)
           double sb = 0.0, sg = 0.0;
 #pragma unroll
           for (int k = 0; k < N; ++k) {
-            sb += tB<Q, N>(t, qz, k) * xr[c][k];
-            sg += tG<Q, N>(t, qz, k) * xr[c][k];
+            sb += tB<Q, N>(t, qz, k) * xv[c][k];
+            sg += tG<Q, N>(t, qz, k) * xv[c][k];
           }
           u[qz * U_QZ * EPB] = sb;
           u[UV + qz * U_QZ * EPB] = sg;
@@ -224,6 +262,8 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::MINB)
       }
     }
     __syncthreads();
+    issue_gather();                             // group grp + grid: lands during F2 / X / B2 / B1
+    load_index(grp + 2 * (int64_t)gridDim.x);   // consumed one group from now
     // ---- F2: y-sweep
     if (r2) {
 #pragma unroll
@@ -298,7 +338,6 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::MINB)
 #pragma unroll
           for (int k = 0; k < N; ++k) W[(c * 3 + v) * WV + ox + k * EPB] = av[c][v][k];
     }
-    gather(grp + gridDim.x);   // next group's z-lines: in flight during B2 / B1
     __syncthreads();
     // QB is free again: stream in the next group's Q-data
     phase ^= 1u;
@@ -351,7 +390,8 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::MINB)
         }
       }
     }
-    __syncthreads();
+    // (no barrier: the top-of-loop barrier orders B1's reads of Bv before
+    // the next F1 writes U)
   }
 }
 
