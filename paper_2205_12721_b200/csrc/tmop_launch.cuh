@@ -8,46 +8,54 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "tmop_apply_xl.cuh"
+#include "tmop_xl.cuh"
 #include "tmop_diag.cuh"
 #include "tmop_elem.cuh"
 #include "tmop_internal.h"
 
 namespace tmop {
 
-// TMOP_APPLY_KERNEL=generic forces the work-item kernel (A/B and parity).
-inline bool force_generic_apply() {
+// TMOP_XL=0 forces the work-item kernels (elem_kernel) everywhere (A/B and
+// parity of the two implementations).
+inline bool xl_enabled() {
   static int v = -1;
   if (v < 0) {
-    const char *e = std::getenv("TMOP_APPLY_KERNEL");
-    v = (e && std::strcmp(e, "generic") == 0) ? 1 : 0;
+    const char *e = std::getenv("TMOP_XL");
+    v = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
   }
   return v == 1;
 }
 
-// 3D Hessian action: the x-line kernel (apply_xl_kernel) where instantiated
-// (p <= 2), else the work-item kernel (elem_kernel<K_APPLY>).  The grid is
-// one persistent wave: 148 SMs x the occupancy the kernel achieves.
-template <int N, int Q, bool NTM>
+template <int KIND>
+constexpr bool xl_kind() {
+  return KIND == K_APPLY || KIND == K_APPLY_NT || KIND == K_GRAD || KIND == K_SETUP || KIND == K_ENERGY ||
+         KIND == K_MINDET;
+}
+
+// 3D x-line kernels (tmop_xl.cuh) where instantiated (p <= 2).  The grid is
+// one persistent wave: SMs x the occupancy the kernel achieves, capped at
+// GRID_CAP (the per-CTA reduction partials).
+template <int N, int Q, int KIND>
 int launch_xl(ElemArgs &a, const Tab &t, cudaStream_t s) {
   using XC = XlCfg<N, Q>;
+  constexpr int smem = XC::template smem<KIND>();
   a.ngroups = (a.ne + XC::EPB - 1) / XC::EPB;
-  a.e_es = 3;
   static_assert(XC::EPB == 8, "e_es assumes 8-element groups");
-  auto kfn = apply_xl_kernel<N, Q, NTM>;
+  if constexpr (xl_backward<KIND>()) a.e_es = 3;
+  auto kfn = xl_kernel<N, Q, KIND>;
   static int per_sm = 0;
   if (per_sm == 0) {
-    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, XC::SMEM) != cudaSuccess) return -2;
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -2;
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, XC::NT, XC::SMEM) != cudaSuccess || nb < 1) nb = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, XC::NT, smem) != cudaSuccess || nb < 1) nb = 1;
     per_sm = nb;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (int)std::min<int64_t>(a.ngroups, (int64_t)sms * per_sm);
+  const int grid = (int)std::min<int64_t>(std::min<int64_t>(a.ngroups, (int64_t)sms * per_sm), GRID_CAP);
   if (grid == 0) return 0;
-  kfn<<<grid, XC::NT, XC::SMEM, s>>>(a, t);
+  kfn<<<grid, XC::NT, smem, s>>>(a, t);
   return grid;
 }
 
@@ -73,8 +81,8 @@ int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
   if constexpr (KIND == K_DIAG || KIND == K_DIAG_NT) {
     return launch_diag<DIM, N, Q, KIND == K_DIAG_NT>(a, t, s);
   } else {
-    if constexpr (DIM == 3 && (KIND == K_APPLY || KIND == K_APPLY_NT) && xl_supported<N, Q>()) {
-      if (!force_generic_apply()) return launch_xl<N, Q, KIND == K_APPLY_NT>(a, t, s);
+    if constexpr (DIM == 3 && xl_kind<KIND>() && xl_supported<N, Q>()) {
+      if (xl_enabled()) return launch_xl<N, Q, KIND>(a, t, s);
     }
     a.ngroups = (a.ne + CF::EPB - 1) / CF::EPB;
     const int grid = (int)std::min<int64_t>(a.ngroups, GRID_CAP);

@@ -1,0 +1,600 @@
+// tmop_xl.cuh -- the 3D element kernels in "x-line" form: the Hessian action
+// (AddMultGradPA, operator.py:401-418), the gradient (AddMultPA,
+// operator.py:328-346), the Hessian setup (AssembleGradPA,
+// operator.py:350-371), the energy (GetLocalStateEnergyPA,
+// operator.py:311-326) and min det(A) (operator.py:296-304).
+//
+// Why this shape (profiles/round1_*.md): on B200 the FP64 pipe is shared by
+// DFMA and DMMA (measured: mixed DFMA+DMMA loops sum to the same ~35 TF/s),
+// so the element contractions stay on DFMA, and the previous work-item
+// kernel was co-limited by shared-memory bandwidth (~6.5 K doubles of
+// shared traffic per p=2 element, 69 % of the LSU wavefront budget) and
+// FP64 issue.  Here one thread owns one x-line (qy, qz) of an element for
+// all three components and keeps, in registers, the y/x-sweep results W, the
+// nine gradient entries of the current point, the point's result (Hessian
+// action / first Piola-Kirchhoff term) and the transposed x-sweep
+// accumulators A -- the quadrature-point fields never touch shared memory.
+// For the Hessian action the group's lean Q-data arrives by one TMA bulk
+// copy issued a group ahead (the lean record stores qx as the slowest point
+// index, lean_slot(), and the element stride is 2 mod 16 doubles, so the X
+// stage reads it conflict-free); the setup writes the record the same way,
+// one coalesced 32-byte run per (element, field, qx) and warp.
+//
+// Layout: a CTA owns EPB = 8 elements per group; thread id = e + 8 * item
+// and every shared buffer is element-interleaved (slot * 8 + e), so a
+// half-warp touches two items x eight elements; the padded strides below
+// make every stage's pair of items differ by an odd number of slots, i.e.
+// every 64-bit shared access is conflict-free.
+//
+// Stages per group (z axis first like contract_dofs_to_quad, fe.py:227-239):
+//   G   all threads:    cp.async gather of the input T-vector (x or v) and the
+//                       fixed flags of the NEXT group into shared memory
+//   F1  item (ky,kx):   z-sweep -> U[c][v][qz][ky][kx], v in {B, G}
+//   X   item (qy,qz):   U -> W (y-sweep of row qy: BB, BG, GB; registers) ->
+//                       gradient at the Q points of the line -> point work
+//                       (KIND) -> A (x^T sweep) -> A[c][v3][qz][qy][kx]
+//   B2  item (qz,kx):   A -> Bv[c][v][qz][ky][kx]   (y^T sweep, fe.py:242-253)
+//   B1  item (ky,kx):   Bv -> element-interleaved E-vector (z^T sweep)
+// B2 / B1 run for the Hessian action and the gradient only.  The E-vector is
+// summed to nodes by e2l_kernel (8-element interleave) in ascending element
+// order, no atomics; energies and min det reduce per CTA in a fixed order.
+#pragma once
+
+#include "tmop_elem.cuh"
+
+namespace tmop {
+
+// Tuning knob (tools/build_variant.sh): occupancy hint (CTAs / SM; 0 = per
+// order default).
+#ifndef TMOP_XL_MINB
+#define TMOP_XL_MINB 0
+#endif
+
+template <int KIND>
+__host__ __device__ constexpr bool xl_backward() {
+  return KIND == K_APPLY || KIND == K_APPLY_NT || KIND == K_GRAD;
+}
+template <int KIND>
+__host__ __device__ constexpr bool xl_qdata() {
+  return KIND == K_APPLY || KIND == K_APPLY_NT;
+}
+
+template <int N, int Q>
+struct XlCfg {
+  static constexpr int EPB = 8;
+  static constexpr int NP = N * N * N, QP = Q * Q * Q;
+  static constexpr int LINES = Q * Q;
+  static constexpr int NT = EPB * LINES;
+  // U / Bv: [c][v][qz][ky*N+kx]          (slots; one slot = EPB doubles)
+  static constexpr int U_QZ = N * N;
+  static constexpr int U_SZ = 6 * Q * U_QZ;
+  // W / A:  [c][v3][qz][qy][kx]
+  static constexpr int W_QY = N | 1;
+  static constexpr int W_QZ0 = Q * W_QY;
+  static constexpr int W_QZ = ((N & 1) || (Q & 1)) ? (W_QZ0 | 1) : W_QZ0;
+  static constexpr int W_SZ = 9 * Q * W_QZ;
+  static constexpr int SLOTS = (U_SZ + W_SZ + 1) & ~1;
+  static constexpr int F = 11;                 // lean fields (T, k0, itau)
+  static constexpr int QS = lean_stride(F * QP);
+  static constexpr int XOFF = SLOTS * EPB;                 // gathered input: XS[c][l][e]
+  static constexpr int FOFF = XOFF + 3 * NP * EPB;         // fixed-flag words: FS[l][e] (uint32)
+  static constexpr int BOFF = FOFF + (NP * EPB + 1) / 2;   // flag byte offsets: FB[l][e] (uint8)
+  static constexpr int QOFF = (BOFF + (NP * EPB + 7) / 8 + 1) & ~1;   // staged Q-data, 16-byte aligned
+  static constexpr int SMEM = (QOFF + EPB * QS) * 8;      // Hessian action
+  // kinds without the A buffer / staged Q-data: U + gather buffers only
+  static constexpr int XOFF_F = U_SZ * EPB;
+  static constexpr int FOFF_F = XOFF_F + 3 * NP * EPB;
+  static constexpr int BOFF_F = FOFF_F + (NP * EPB + 1) / 2;
+  static constexpr int SMEM_F = (BOFF_F + (NP * EPB + 7) / 8 + 1) * 8;
+  // setup: the group's lean records are assembled in shared memory and
+  // written back by one TMA bulk store
+  static constexpr int QOFF_S = (BOFF_F + (NP * EPB + 7) / 8 + 1) & ~1;
+  static constexpr int SMEM_S = (QOFF_S + EPB * QS) * 8;
+  template <int KIND>
+  static constexpr int smem() {
+    return xl_qdata<KIND>() ? SMEM : (xl_backward<KIND>() ? QOFF * 8 : (KIND == K_SETUP ? SMEM_S : SMEM_F));
+  }
+  static constexpr int GJ = (EPB * NP + NT - 1) / NT;      // gather (element, node) pairs per thread
+  // CTAs / SM: the backward kinds keep ~110 doubles live in the x-line
+  // (p = 2: ~240 registers); forward-only kinds ~half
+  static constexpr int WARPS = (NT + 31) / 32;
+  template <int KIND>
+  static constexpr int minb() {
+    return TMOP_XL_MINB ? TMOP_XL_MINB
+                        : cmax(1, 65536 / (WARPS * 32 * (xl_backward<KIND>() ? (N <= 2 ? 168 : 248) : 128)));
+  }
+};
+
+template <int N, int Q>
+__host__ __device__ constexpr bool xl_supported() {
+  // register / shared-memory budget: p = 1, 2 (the x-line keeps 18 N
+  // doubles of W and A live across the point loop) and the CTA's work
+  // buffers + staged Q-data within 227 KB
+  return N <= 3 && Q >= 2 && XlCfg<N, Q>::SMEM <= 227 * 1024;
+}
+
+// Fixed-order block reductions for any CTA size (partial warps allowed):
+// every thread stores its partial, thread 0 combines them in thread order.
+template <int NT>
+__device__ __forceinline__ double xl_block_sum(double v, double *sv) {
+  __syncthreads();
+  sv[threadIdx.x] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NT; ++i) r += sv[i];
+  return r;
+}
+template <int NT>
+__device__ __forceinline__ MinLoc xl_block_minloc(MinLoc m, double *sv, int64_t *si) {
+  __syncthreads();
+  sv[threadIdx.x] = m.v;
+  si[threadIdx.x] = m.i;
+  __syncthreads();
+  MinLoc r{DBL_MAX, LLONG_MAX};
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NT; ++i) r = minloc(r, MinLoc{sv[i], si[i]});
+  return r;
+}
+
+// A:B as three row sums added pairwise (dependency depth 4 instead of 9).
+__device__ __forceinline__ double tdot(const double (&A)[3][3], const double (&B)[3][3]) {
+  double r[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r[i] = A[i][0] * B[i][0] + A[i][1] * B[i][1] + A[i][2] * B[i][2];
+  return (r[0] + r[1]) + r[2];
+}
+
+// Point stage of the x-line: z = (scaled d2mu/dT2) : g from the lean record
+// (T, k0, itau), accumulated straight into the transposed x-sweep:
+// av[c][0][k] += G(qx,k) z[c][0], av[c][v][k] += B(qx,k) z[c][v] (v = 1, 2).
+// Template metrics: S = itau cof(T) is folded into the coefficients and the
+// block (_kernels.py:235-258) is applied with C = cof(T) directly.
+template <int N, bool NTM>
+__device__ __forceinline__ void xl_point(int metric, const double (&qd)[11], const double (&g)[3][3],
+                                         const double (&tg)[N], const double (&tb)[N], double (&av)[3][3][N]) {
+  double T[3][3], C[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) T[i][j] = qd[i * 3 + j];
+  mcof<3>(T, C);
+  auto acc = [&](int c, int n, double z) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) av[c][n][k] += (n == 0 ? tg[k] : tb[k]) * z;
+  };
+  if constexpr (!NTM) {
+    const double k0 = qd[9], itau = qd[10];
+    double c[4];
+    lean_coeffs(metric, k0, itau, tdot(T, T), c);
+    const double dt = tdot(T, g);
+    const double ds = itau * tdot(C, g);
+    const double w1 = (c[1] * dt + c[2] * ds) * itau;
+    const double w2 = c[1] * ds;
+    const double c3 = c[3] * (itau * itau);
+    double gs[3][3];
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int n = 0; n < 3; ++n) gs[p][n] = g[0][p] * C[0][n] + g[1][p] * C[1][n] + g[2][p] * C[2][n];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int n = 0; n < 3; ++n) {
+        const double cross = C[a][0] * gs[0][n] + C[a][1] * gs[1][n] + C[a][2] * gs[2][n];
+        acc(a, n, c[0] * g[a][n] + w1 * C[a][n] + w2 * T[a][n] + c3 * cross);
+      }
+  } else {
+    double S[3][3], z[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) S[i][j] = C[i][j] * qd[10];
+    nt_hess<3>(metric, qd[9], S, T, g, z);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int n = 0; n < 3; ++n) acc(a, n, z[a][n]);
+  }
+}
+
+// cp.async (LDGSTS): global -> shared without register staging.
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// TMA bulk store shared -> global (bulk_group completion) and its fences.
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_store(void *dst, const void *src, uint32_t bytes) {
+  asm volatile(
+      "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+      "cp.async.bulk.commit_group;" ::"l"(dst),
+      "r"(smem_u32(src)), "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// x-line point work of the forward-only / gradient kinds at one point:
+// J = the Jacobian dx/dxi (operator.py:252-292 restated like the work-item
+// kernel's point stage, same operation order).
+template <int KIND, int N, int Q>
+__device__ __forceinline__ void xl_point_x(const ElemArgs &a, const Tab &t, int64_t eg, int line, int qx,
+                                           const double (&J)[3][3], const double (&tg)[N], const double (&tb)[N],
+                                           double (&av)[3][3][N], double &acc, MinLoc &mn, double *rec) {
+  constexpr int QP = Q * Q * Q;
+  const int q = qx + Q * line;                       // reference point index (x fastest)
+  const double dj = mdet<3>(J);
+  if (eg < a.ne) mn = minloc(mn, MinLoc{dj, eg * QP + q});
+  if constexpr (KIND == K_SETUP || KIND == K_GRAD || KIND == K_ENERGY) {
+    const double tau = dj * a.inv_s_d;
+    const double I1 = mfro2<3>(J) * (a.inv_s * a.inv_s);
+    const double cs = a.inv_s_dm1 / tau;
+    double Cof[3][3];
+    mcof<3>(J, Cof);
+    double S[3][3], T[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        S[i][j] = cs * Cof[i][j];
+        T[i][j] = a.inv_s * J[i][j];
+      }
+    const double wpt = wq<3, Q>(t, q);
+    if constexpr (KIND == K_ENERGY) {
+      if (eg < a.ne) acc += wpt * metric_mu<3>(a.metric, tau, I1, S);
+    } else if constexpr (KIND == K_SETUP) {
+      // lean record (operator.py:350-371 restated; see lean_k0), staged in
+      // shared memory at slot = line + Q^2 qx of this thread's element
+      double *qo = rec + line + Q * Q * qx;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) qo[(i * 3 + j) * QP] = T[i][j];
+      qo[9 * QP] = lean_k0(a.metric, a.coef_h * wpt, tau);
+      qo[10 * QP] = 1.0 / tau;
+    } else {  // K_GRAD: P = cw (a_t T + a_s S) (operator.py:328-346)
+      const double cw = a.coef_g * wpt;
+      double P[3][3];
+      if (metric_is_template(a.metric)) {
+        double at, as;
+        metric_first_coeffs(a.metric, tau, I1, at, as);
+        const double ct = cw * at * a.inv_s;
+        const double cc = cw * as * a.inv_s_dm1 / tau;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) P[i][j] = ct * J[i][j] + cc * Cof[i][j];
+      } else {
+        nt_first<3>(a.metric, T, S, P);
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) P[i][j] *= cw;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          av[c][0][k] += tg[k] * P[c][0];
+          av[c][1][k] += tb[k] * P[c][1];
+          av[c][2][k] += tb[k] * P[c][2];
+        }
+    }
+  } else if constexpr (KIND == K_VOLUME) {
+    if (eg < a.ne) acc += dj * wq<3, Q>(t, q);
+  }
+}
+
+
+template <int N, int Q, int KIND>
+__global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KIND>())
+    xl_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
+  using XC = XlCfg<N, Q>;
+  constexpr bool APPLY = xl_qdata<KIND>();
+  constexpr bool BACK = xl_backward<KIND>();
+  constexpr bool MASK = APPLY;          // the apply zeroes constrained inputs (operator.py:409)
+  constexpr bool NTM = KIND == K_APPLY_NT;
+  constexpr bool RSUM = KIND == K_ENERGY || KIND == K_VOLUME;
+  constexpr bool RMIN = KIND == K_SETUP || KIND == K_GRAD || KIND == K_ENERGY || KIND == K_MINDET;
+  constexpr int EPB = XC::EPB, NP = XC::NP, QP = XC::QP, QS = XC::QS, NT = XC::NT;
+  constexpr int U_QZ = XC::U_QZ, W_QY = XC::W_QY, W_QZ = XC::W_QZ;
+  constexpr int XOFF = BACK ? XC::XOFF : XC::XOFF_F;
+  constexpr int FOFF = BACK ? XC::FOFF : XC::FOFF_F;
+  constexpr int BOFF = BACK ? XC::BOFF : XC::BOFF_F;
+  extern __shared__ __align__(16) double smem[];
+  double *U = smem;                       // U / Bv
+  double *W = smem + XC::U_SZ * EPB;      // A (backward kinds)
+  double *QB = smem + (KIND == K_SETUP ? XC::QOFF_S : XC::QOFF);   // the group's lean Q-data (TMA-staged)
+  __shared__ __align__(8) uint64_t qbar;
+  __shared__ double red_v[(RSUM || RMIN) ? NT : 1];
+  __shared__ int64_t red_i[RMIN ? NT : 1];
+
+  const int tid = threadIdx.x;
+  const int e = tid % EPB;                // element slot of this thread (all stages)
+  const int item = tid / EPB;
+  double *QS_rec = QB + e * QS;           // setup: this thread's staged element record
+
+  // per-stage roles (loop-invariant)
+  const bool r1 = item < N * N;                 // F1 / B1: (ky, kx)
+  const bool r2 = item < Q * N;                 // B2: (qz, kx)
+  const int i2_kx = item % N, i2_qz = item / N;
+  const int lqy = item % Q, lqz = item / Q;     // X stage: line (qy, qz); all threads
+  const int line = item;
+
+  // shared offsets (doubles) of each stage's item base
+  const int o1 = item * EPB + e;                                     // U[..][qz=0][item]
+  const int o2u = (i2_qz * U_QZ + i2_kx) * EPB + e;                 // U[..][qz][ky=0][kx]
+  const int o2w = (i2_qz * W_QZ + i2_kx) * EPB + e;                 // A[..][qz][qy=0][kx]
+  const int ox = (lqz * W_QZ + lqy * W_QY) * EPB + e;               // A[..][qz][qy][k=0]
+  const int ou = lqz * U_QZ * EPB + e;                              // U[..][qz][ky=0][kx=0]
+  double ty_b[N], ty_g[N];                                          // B, G rows of qy
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    ty_b[k] = t.B[lqy * N + k];
+    ty_g[k] = t.G[lqy * N + k];
+  }
+  constexpr int UV = Q * U_QZ * EPB;      // U stride of v (c stride = 2 UV)
+  constexpr int WV = Q * W_QZ * EPB;      // A stride of v3 (c stride = 3 WV)
+
+  // ---- gather: asynchronous.  Every thread owns GJ (element, local node)
+  // pairs of a group (element-fastest, matching the interleaved buffers);
+  // the restriction indices of group g + 2 are loaded during group g, and
+  // once F1 has consumed the gather buffer, cp.async copies in[c][node] (and,
+  // for the apply, the 4-byte word holding fixed[node]) of group g + 1
+  // straight into shared memory, landing during X / B2 / B1.
+  double *XS = smem + XOFF;
+  uint32_t *FS = reinterpret_cast<uint32_t *>(smem + FOFF);
+  uint8_t *FB = reinterpret_cast<uint8_t *>(smem + BOFF);
+  int nd[XC::GJ];
+  auto load_index = [&](int64_t grp) {
+#pragma unroll
+    for (int j = 0; j < XC::GJ; ++j) {
+      const int w = tid + j * NT;
+      const int64_t eg = grp * EPB + w % EPB;
+      nd[j] = (w < EPB * NP && grp < a.ngroups && eg < a.ne) ? __ldg(a.restr + eg * NP + w / EPB) : -1;
+    }
+  };
+  auto issue_gather = [&]() {
+#pragma unroll
+    for (int j = 0; j < XC::GJ; ++j) {
+      const int w = tid + j * NT;
+      if (nd[j] >= 0) {
+        const int ge = w % EPB, l = w / EPB;
+        const int64_t node = nd[j];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cp_async8(XS + (c * NP + l) * EPB + ge, a.in + c * a.nn + node);
+        if constexpr (MASK) {
+          cp_async4(FS + l * EPB + ge, reinterpret_cast<const uint32_t *>(a.fixed + (node & ~(int64_t)3)));
+          FB[l * EPB + ge] = (uint8_t)(8 * (node & 3));
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  // ---- lean Q-data (apply): the group's EPB contiguous element records are
+  // streamed into QB by one TMA bulk copy, issued one group ahead (after the
+  // X stage has consumed the previous group's copy).
+  auto issue = [&](int64_t grp) {
+    const int64_t e0 = grp * EPB;
+    const int64_t cnt = (a.ne - e0) < EPB ? (a.ne - e0) : EPB;
+    const uint32_t bytes = (uint32_t)(cnt * QS * 8);
+    mbar_expect_tx(&qbar, bytes);
+    tma_load_1d(QB, a.qdata + e0 * QS, bytes, &qbar);
+  };
+  const double *qb = QB + e * QS + lqy + Q * lqz;   // field 0 of point (qx = 0) of this line
+  auto qload = [&](int qx, double (&qd)[11]) {
+#pragma unroll
+    for (int f = 0; f < 11; ++f) qd[f] = qb[f * QP + Q * Q * qx];
+  };
+  uint32_t phase = 0;
+  if constexpr (APPLY) {
+    if (tid == 0) {
+      mbar_init(&qbar, 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (tid == 0 && (int64_t)blockIdx.x < a.ngroups) issue(blockIdx.x);
+  }
+  double acc = 0.0;
+  MinLoc mn{DBL_MAX, LLONG_MAX};
+
+  load_index(blockIdx.x);
+  issue_gather();
+  load_index((int64_t)blockIdx.x + gridDim.x);
+  for (int64_t grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
+    const int64_t eg = grp * EPB + e;
+    if constexpr (KIND == K_SETUP) {
+      if (tid == 0) bulk_wait_read();   // previous group's record store has read QB
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- F1: z-sweep of the gathered z-lines
+    if (r1) {
+      double xv[3][N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const int l = k * N * N + item;
+        if constexpr (MASK) {
+          const uint32_t fw = FS[l * EPB + e] >> FB[l * EPB + e];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) xv[c][k] = ((fw >> c) & 1u) ? 0.0 : XS[(c * NP + l) * EPB + e];
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) xv[c][k] = XS[(c * NP + l) * EPB + e];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double *u = U + c * 2 * UV + o1;
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          double sb = 0.0, sg = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            sb += tB<Q, N>(t, qz, k) * xv[c][k];
+            sg += tG<Q, N>(t, qz, k) * xv[c][k];
+          }
+          u[qz * U_QZ * EPB] = sb;
+          u[UV + qz * U_QZ * EPB] = sg;
+        }
+      }
+    }
+    __syncthreads();
+    issue_gather();                             // group grp + grid: lands during X / B2 / B1
+    load_index(grp + 2 * (int64_t)gridDim.x);   // consumed one group from now
+    if constexpr (APPLY) mbar_wait(&qbar, phase);   // this group's Q-data
+    // ---- X: y-sweep of this line's row qy, x-sweep, point stage,
+    // transposed x-sweep -- all in registers
+    {
+      double wv[3][3][N], av[3][3][N];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double *ub = U + c * 2 * UV + ou;
+#pragma unroll
+        for (int kx = 0; kx < N; ++kx) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+          for (int ky = 0; ky < N; ++ky) {
+            const double vb = ub[(ky * N + kx) * EPB], vg = ub[UV + (ky * N + kx) * EPB];
+            s0 += ty_b[ky] * vb;
+            s1 += ty_g[ky] * vb;
+            s2 += ty_b[ky] * vg;
+          }
+          wv[c][0][kx] = s0;
+          wv[c][1][kx] = s1;
+          wv[c][2][kx] = s2;
+          av[c][0][kx] = av[c][1][kx] = av[c][2][kx] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        double tg[N], tb[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          tg[k] = tG<Q, N>(t, qx, k);
+          tb[k] = tB<Q, N>(t, qx, k);
+        }
+        double g[3][3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            s0 += tg[k] * wv[c][0][k];
+            s1 += tb[k] * wv[c][1][k];
+            s2 += tb[k] * wv[c][2][k];
+          }
+          g[c][0] = s0;
+          g[c][1] = s1;
+          g[c][2] = s2;
+        }
+        if constexpr (APPLY) {
+          double qd[11];
+          qload(qx, qd);
+          xl_point<N, NTM>(a.metric, qd, g, tg, tb, av);
+        } else {
+          xl_point_x<KIND, N, Q>(a, t, eg, line, qx, g, tg, tb, av, acc, mn, QS_rec);
+        }
+      }
+      if constexpr (BACK) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int v = 0; v < 3; ++v)
+#pragma unroll
+            for (int k = 0; k < N; ++k) W[(c * 3 + v) * WV + ox + k * EPB] = av[c][v][k];
+      }
+    }
+    if constexpr (BACK) {
+      __syncthreads();
+      if constexpr (APPLY) {
+        // QB is free again: stream in the next group's Q-data
+        phase ^= 1u;
+        if (tid == 0 && grp + gridDim.x < a.ngroups) issue(grp + gridDim.x);
+      }
+      // ---- B2: y^T sweep  A -> Bv (U region)
+      if (r2) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double *A = W + c * 3 * WV + o2w;
+          double a0[Q], a1[Q], a2[Q];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            a0[q] = A[q * W_QY * EPB];
+            a1[q] = A[WV + q * W_QY * EPB];
+            a2[q] = A[2 * WV + q * W_QY * EPB];
+          }
+          double *b = U + c * 2 * UV + o2u;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+              s0 += tB<Q, N>(t, q, k) * a0[q] + tG<Q, N>(t, q, k) * a1[q];
+              s1 += tB<Q, N>(t, q, k) * a2[q];
+            }
+            b[k * N * EPB] = s0;
+            b[UV + k * N * EPB] = s1;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- B1: z^T sweep -> element-interleaved E-vector
+      if (r1) {
+        double *out = a.E + (grp * 3 * NP + item) * EPB + e;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double *b = U + c * 2 * UV + o1;
+          double b0[Q], b1[Q];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            b0[q] = b[q * U_QZ * EPB];
+            b1[q] = b[UV + q * U_QZ * EPB];
+          }
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) s += tB<Q, N>(t, q, k) * b0[q] + tG<Q, N>(t, q, k) * b1[q];
+            out[(c * NP + k * N * N) * EPB] = s;
+          }
+        }
+      }
+    }
+    if constexpr (KIND == K_SETUP) {
+      // the group's records are complete in QB: one TMA bulk store
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        const int64_t e0 = grp * EPB;
+        const int64_t cnt = (a.ne - e0) < EPB ? (a.ne - e0) : EPB;
+        bulk_store(a.qout + e0 * QS, QB, (uint32_t)(cnt * QS * 8));
+      }
+    }
+    // (no end-of-group barrier: the top-of-loop barrier orders this group's
+    // reads of U / Bv before the next F1 writes U)
+  }
+  if constexpr (KIND == K_SETUP) {
+    if (tid == 0) bulk_wait_all();
+  }
+
+  // ---- per-CTA deterministic partials
+  if constexpr (RSUM) {
+    const double sum = xl_block_sum<NT>(acc, red_v);
+    if (tid == 0) a.part_sum[blockIdx.x] = sum;
+  }
+  if constexpr (RMIN) {
+    const MinLoc m = xl_block_minloc<NT>(mn, red_v, red_i);
+    if (tid == 0) {
+      a.part_min[blockIdx.x] = m.v;
+      a.part_arg[blockIdx.x] = m.i;
+    }
+  }
+}
+
+}  // namespace tmop
