@@ -209,7 +209,7 @@ int tmop_qdata_fields(const tmop_ctx *c) {
 
 int64_t tmop_qdata_stride(const tmop_ctx *c) {
   if (!c) return -1;
-  return lean_stride(tmop_qdata_fields(c) * c->QP);
+  return lean_stride(tmop_qdata_fields(c) * c->QP, xl_epb(c->n1));
 }
 
 int64_t tmop_qdata_size(const tmop_ctx *c) {

@@ -59,12 +59,18 @@ __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * i
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int cclamp(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// Element-group size of the 3D x-line kernels (tmop_xl.cuh): 8 elements per
+// CTA for p <= 2, 4 for p >= 3 (shared-memory budget).
+__host__ __device__ constexpr int xl_epb(int n1) { return n1 <= 3 ? 8 : 4; }
+
 // Element stride of the lean Q-data record (doubles): the smallest value
-// >= fields * points with stride == 2 (mod 16).  Even, so every element
-// block is 16-byte aligned (TMA bulk copies), and == 2 (mod 16) so that 8
-// element-interleaved threads reading the same field/slot of 8 consecutive
-// staged elements hit 8 distinct bank pairs (apply_xl_kernel).
-__host__ __device__ constexpr int lean_stride(int n) { return n + ((18 - n % 16) % 16); }
+// >= fields * points with stride == 16 / epb (mod 16).  Even, so every
+// element block is 16-byte aligned (TMA bulk copies), and with that residue
+// the epb element-interleaved threads of a half-warp reading the same
+// field / slot of consecutive staged elements hit distinct bank pairs.
+__host__ __device__ constexpr int lean_stride(int n, int epb) {
+  return n + ((16 + 16 / epb - n % 16) % 16);
+}
 
 template <int DIM, int N, int Q>
 struct Cfg {
@@ -99,7 +105,7 @@ struct Cfg {
   // lean Q-data: T (d*d), k0, itau per point; element stride rounded to an
   // even number of doubles so every element block is 16-byte aligned (TMA).
   static constexpr int F = DIM * DIM + 2;
-  static constexpr int QS = lean_stride(F * QP);
+  static constexpr int QS = lean_stride(F * QP, xl_epb(N));
   // Launch shape, from the A/B sweep of round 1 (profiles/round1_apply_ab.md):
   // 128-thread CTAs with ~56 KB (4 CTAs / SM) for p = 1, 2, 4; 256-thread
   // CTAs with ~72 KB (3 CTAs / SM) for p = 3.

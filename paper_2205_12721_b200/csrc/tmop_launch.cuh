@@ -26,13 +26,18 @@ inline bool xl_enabled() {
   return v == 1;
 }
 
-template <int KIND>
+// Which kinds run in x-line form, per order (measured, profiles/round1_*):
+// p <= 3 all of them; p = 4 only the forward-only energy / min det -- its
+// backward kinds and setup keep ~90+ doubles live per line and spill, and
+// the work-item kernel is faster there.
+template <int N, int KIND>
 constexpr bool xl_kind() {
+  if constexpr (N >= 5) return KIND == K_ENERGY || KIND == K_MINDET;
   return KIND == K_APPLY || KIND == K_APPLY_NT || KIND == K_GRAD || KIND == K_SETUP || KIND == K_ENERGY ||
          KIND == K_MINDET;
 }
 
-// 3D x-line kernels (tmop_xl.cuh) where instantiated (p <= 2).  The grid is
+// 3D x-line kernels (tmop_xl.cuh) where selected (xl_kind) and the CTA fits.  The grid is
 // one persistent wave: SMs x the occupancy the kernel achieves, capped at
 // GRID_CAP (the per-CTA reduction partials).
 template <int N, int Q, int KIND>
@@ -40,8 +45,8 @@ int launch_xl(ElemArgs &a, const Tab &t, cudaStream_t s) {
   using XC = XlCfg<N, Q>;
   constexpr int smem = XC::template smem<KIND>();
   a.ngroups = (a.ne + XC::EPB - 1) / XC::EPB;
-  static_assert(XC::EPB == 8, "e_es assumes 8-element groups");
-  if constexpr (xl_backward<KIND>()) a.e_es = 3;
+  static_assert(XC::EPB == 8 || XC::EPB == 4, "e_es assumes 4- or 8-element groups");
+  if constexpr (xl_backward<KIND>()) a.e_es = XC::EPB == 8 ? 3 : 2;
   auto kfn = xl_kernel<N, Q, KIND>;
   static int per_sm = 0;
   if (per_sm == 0) {
@@ -81,7 +86,7 @@ int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
   if constexpr (KIND == K_DIAG || KIND == K_DIAG_NT) {
     return launch_diag<DIM, N, Q, KIND == K_DIAG_NT>(a, t, s);
   } else {
-    if constexpr (DIM == 3 && xl_kind<KIND>() && xl_supported<N, Q>()) {
+    if constexpr (DIM == 3 && xl_kind<N, KIND>() && xl_supported<N, Q>()) {
       if (xl_enabled()) return launch_xl<N, Q, KIND>(a, t, s);
     }
     a.ngroups = (a.ne + CF::EPB - 1) / CF::EPB;

@@ -20,11 +20,11 @@
 // stage reads it conflict-free); the setup writes the record the same way,
 // one coalesced 32-byte run per (element, field, qx) and warp.
 //
-// Layout: a CTA owns EPB = 8 elements per group; thread id = e + 8 * item
-// and every shared buffer is element-interleaved (slot * 8 + e), so a
-// half-warp touches two items x eight elements; the padded strides below
-// make every stage's pair of items differ by an odd number of slots, i.e.
-// every 64-bit shared access is conflict-free.
+// Layout: a CTA owns EPB = 8 (p <= 2) or 4 (p >= 3) elements per group;
+// thread id = e + EPB * item and every shared buffer is element-interleaved
+// (slot * EPB + e), so a half-warp touches 16 / EPB items x EPB elements;
+// the padded strides (XlPad, searched by tools/xl_banks.py) make every 64-bit
+// shared access pattern of the kernel conflict-free.
 //
 // Stages per group (z axis first like contract_dofs_to_quad, fe.py:227-239):
 //   G   all threads:    cp.async gather of the input T-vector (x or v) and the
@@ -36,7 +36,7 @@
 //   B2  item (qz,kx):   A -> Bv[c][v][qz][ky][kx]   (y^T sweep, fe.py:242-253)
 //   B1  item (ky,kx):   Bv -> element-interleaved E-vector (z^T sweep)
 // B2 / B1 run for the Hessian action and the gradient only.  The E-vector is
-// summed to nodes by e2l_kernel (8-element interleave) in ascending element
+// summed to nodes by e2l_kernel (EPB-element interleave) in ascending element
 // order, no atomics; energies and min det reduce per CTA in a fixed order.
 #pragma once
 
@@ -59,23 +59,33 @@ __host__ __device__ constexpr bool xl_qdata() {
   return KIND == K_APPLY || KIND == K_APPLY_NT;
 }
 
+// Padded strides (in slots) chosen by tools/xl_banks.py so that every shared
+// access pattern of the kernel is bank-conflict free for the group size.
+template <int N, int Q>
+struct XlPad {
+  static constexpr int EPB = xl_epb(N);
+  static constexpr int U_QZ = EPB == 8 ? (N * N) | (Q & 1) : (N == 4 ? (Q % 4 == 0 ? 16 : 17) : 25);
+  static constexpr int W_QY = EPB == 8 ? (N | 1) : ((N == 5 && (Q == 3 || Q == 7)) ? 7 : 5);
+  static constexpr int W_QZ = EPB == 8 ? Q * W_QY + ((N & 1) && !(Q & 1) ? 1 : 0)
+                                       : (N == 4 ? Q * 5 : (Q == 3 ? 21 : Q == 4 ? 21 : Q == 6 ? 33 : Q * W_QY));
+};
+
 template <int N, int Q>
 struct XlCfg {
-  static constexpr int EPB = 8;
+  static constexpr int EPB = XlPad<N, Q>::EPB;
   static constexpr int NP = N * N * N, QP = Q * Q * Q;
   static constexpr int LINES = Q * Q;
   static constexpr int NT = EPB * LINES;
   // U / Bv: [c][v][qz][ky*N+kx]          (slots; one slot = EPB doubles)
-  static constexpr int U_QZ = N * N;
+  static constexpr int U_QZ = XlPad<N, Q>::U_QZ;
   static constexpr int U_SZ = 6 * Q * U_QZ;
   // W / A:  [c][v3][qz][qy][kx]
-  static constexpr int W_QY = N | 1;
-  static constexpr int W_QZ0 = Q * W_QY;
-  static constexpr int W_QZ = ((N & 1) || (Q & 1)) ? (W_QZ0 | 1) : W_QZ0;
+  static constexpr int W_QY = XlPad<N, Q>::W_QY;
+  static constexpr int W_QZ = XlPad<N, Q>::W_QZ;
   static constexpr int W_SZ = 9 * Q * W_QZ;
   static constexpr int SLOTS = (U_SZ + W_SZ + 1) & ~1;
   static constexpr int F = 11;                 // lean fields (T, k0, itau)
-  static constexpr int QS = lean_stride(F * QP);
+  static constexpr int QS = lean_stride(F * QP, EPB);
   static constexpr int XOFF = SLOTS * EPB;                 // gathered input: XS[c][l][e]
   static constexpr int FOFF = XOFF + 3 * NP * EPB;         // fixed-flag words: FS[l][e] (uint32)
   static constexpr int BOFF = FOFF + (NP * EPB + 1) / 2;   // flag byte offsets: FB[l][e] (uint8)
@@ -101,16 +111,16 @@ struct XlCfg {
   template <int KIND>
   static constexpr int minb() {
     return TMOP_XL_MINB ? TMOP_XL_MINB
-                        : cmax(1, 65536 / (WARPS * 32 * (xl_backward<KIND>() ? (N <= 2 ? 168 : 248) : 128)));
+                        : cmax(1, 65536 / (WARPS * 32 *
+                                           (xl_backward<KIND>() ? (N <= 2 ? 168 : N == 3 ? 248 : 255)
+                                                                : (N <= 3 ? 128 : 168))));
   }
 };
 
 template <int N, int Q>
 __host__ __device__ constexpr bool xl_supported() {
-  // register / shared-memory budget: p = 1, 2 (the x-line keeps 18 N
-  // doubles of W and A live across the point loop) and the CTA's work
-  // buffers + staged Q-data within 227 KB
-  return N <= 3 && Q >= 2 && XlCfg<N, Q>::SMEM <= 227 * 1024;
+  // the CTA's work buffers + staged Q-data within 227 KB
+  return Q >= 2 && XlCfg<N, Q>::SMEM <= 227 * 1024;
 }
 
 // Fixed-order block reductions for any CTA size (partial warps allowed):
