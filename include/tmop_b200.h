@@ -80,6 +80,14 @@ int tmop_ctx_destroy(tmop_ctx *ctx);
 int tmop_ctx_set_stream(tmop_ctx *ctx, void *stream);
 /* Change target scale (build_targets, metrics.py:333-345) after creation. */
 int tmop_ctx_set_target(tmop_ctx *ctx, double inv_scale, double det_w);
+
+/* Declare that the mesh is the (nx, ny, nz) box lattice of build_box
+ * (mesh.py:118-164).  The restriction is verified on the device; when it
+ * matches, *accepted = 1 and the E->L gathers enumerate each node's element
+ * copies arithmetically (same ascending element order, bitwise identical
+ * sums) instead of reading the transpose map.  3D only; otherwise
+ * *accepted = 0 and nothing changes.  Synchronises the context stream. */
+int tmop_ctx_set_lattice(tmop_ctx *ctx, int nx, int ny, int nz, int *accepted);
 int tmop_qdata_fields(const tmop_ctx *ctx);            /* doubles per point   */
 int64_t tmop_qdata_stride(const tmop_ctx *ctx);        /* doubles per element */
 int64_t tmop_qdata_size(const tmop_ctx *ctx);          /* doubles total       */

@@ -51,6 +51,10 @@ struct tmop_ctx {
   double *part_sum, *part_min;
   int64_t *part_arg;
   double *vpart1, *vpart2;
+  int lat_n[3], lat_p;   // verified box lattice (tmop_ctx_set_lattice), lat_p = 0: none
+  uint64_t mag_x, mag_y;
+  int sh_x, sh_y;
+  int *flag;             // device scratch word
   double *hist;      // MINRES residual history (device, optional)
   int hist_cap;
 };
@@ -104,6 +108,21 @@ static ElemArgs base_args(const tmop_ctx *c) {
   a.part_min = c->part_min;
   a.part_arg = c->part_arg;
   return a;
+}
+
+static E2LMap e2l_map(const tmop_ctx *c) {
+  E2LMap m;
+  m.off = c->l2e_off;
+  m.idx = c->l2e_idx;
+  m.np = c->NP;
+  m.es = c->e_es;
+  for (int i = 0; i < 3; ++i) m.lat_n[i] = c->lat_n[i];
+  m.lat_p = c->lat_p;
+  m.mag_x = c->mag_x;
+  m.mag_y = c->mag_y;
+  m.sh_x = c->sh_x;
+  m.sh_y = c->sh_y;
+  return m;
 }
 
 static int run(tmop_ctx *c, int kind, ElemArgs &a, int *grid_out) {
@@ -168,6 +187,7 @@ int tmop_ctx_create(tmop_ctx **out, int dim, int order, int n_quad, int64_t n_el
   if (e == cudaSuccess) e = cudaMalloc(&c->part_arg, GRID_CAP * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->vpart1, VEC_GRID_CAP * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->vpart2, VEC_GRID_CAP * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c->flag, sizeof(int));
   if (e != cudaSuccess) {
     tmop_ctx_destroy(c);
     return fail(TMOP_ERR_CUDA, "workspace allocation failed: %s", cudaGetErrorString(e));
@@ -184,6 +204,7 @@ int tmop_ctx_destroy(tmop_ctx *c) {
   cudaFree(c->part_arg);
   cudaFree(c->vpart1);
   cudaFree(c->vpart2);
+  cudaFree(c->flag);
   delete c;
   return TMOP_OK;
 }
@@ -191,6 +212,39 @@ int tmop_ctx_destroy(tmop_ctx *c) {
 int tmop_ctx_set_stream(tmop_ctx *c, void *stream) {
   if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
   c->stream = (cudaStream_t)stream;
+  return TMOP_OK;
+}
+
+int tmop_ctx_set_lattice(tmop_ctx *c, int nx, int ny, int nz, int *accepted) {
+  if (!c || !accepted) return fail(TMOP_ERR_ARG, "NULL argument");
+  *accepted = 0;
+  c->lat_p = 0;
+  const int p = c->order;
+  if (c->dim != 3 || nx < 1 || ny < 1 || nz < 1) return TMOP_OK;
+  if ((int64_t)nx * ny * nz != c->ne) return TMOP_OK;
+  if (((int64_t)nx * p + 1) * ((int64_t)ny * p + 1) * ((int64_t)nz * p + 1) != c->nn) return TMOP_OK;
+  if (c->nn >= (int64_t)1 << 31 || c->ne >= (int64_t)1 << 31) return TMOP_OK;   // 32-bit lattice arithmetic
+  CUDA_TRY(cudaMemsetAsync(c->flag, 0, sizeof(int), c->stream));
+  launch_lattice_check(c->ne, c->NP, c->restr, nx, ny, nz, p, c->flag, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  int bad = 1;
+  CUDA_TRY(cudaMemcpyAsync(&bad, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (bad) return TMOP_OK;
+  c->lat_n[0] = nx;
+  c->lat_n[1] = ny;
+  c->lat_n[2] = nz;
+  c->lat_p = p;
+  // magic numbers for exact n / d with n < 2^31: l = ceil(log2 d), mag = ceil(2^(32+l) / d)
+  auto magic = [](uint64_t d, uint64_t &mag, int &sh) {
+    int l = 0;
+    while (((uint64_t)1 << l) < d) ++l;
+    sh = 32 + l;
+    mag = (((uint64_t)1 << sh) + d - 1) / d;
+  };
+  magic((uint64_t)nx * p + 1, c->mag_x, c->sh_x);
+  magic((uint64_t)ny * p + 1, c->mag_y, c->sh_y);
+  *accepted = 1;
   return TMOP_OK;
 }
 
@@ -262,7 +316,7 @@ int tmop_hessian_apply(tmop_ctx *c, const double *qdata, const double *v, double
   a.qdata = qdata;
   int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
   if (rc) return rc;
-  launch_e2l(c->dim, c->nn, c->NP, c->e_es, c->l2e_off, c->l2e_idx, c->E, c->fixed, 0, v, nullptr, y, c->stream);
+  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 0, v, nullptr, y, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }
@@ -277,7 +331,7 @@ int tmop_hessian_apply_elements(tmop_ctx *c, const double *qdata, const double *
 
 int tmop_hessian_apply_gather(tmop_ctx *c, const double *v, double *y) {
   if (!c || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
-  launch_e2l(c->dim, c->nn, c->NP, c->e_es, c->l2e_off, c->l2e_idx, c->E, c->fixed, 0, v, nullptr, y, c->stream);
+  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 0, v, nullptr, y, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }
@@ -288,7 +342,7 @@ int tmop_hessian_diagonal(tmop_ctx *c, const double *qdata, double *diag) {
   a.qdata = qdata;
   int rc = run(c, metric_is_template(c->metric) ? K_DIAG : K_DIAG_NT, a, nullptr);
   if (rc) return rc;
-  launch_e2l(c->dim, c->nn, c->NP, c->e_es, c->l2e_off, c->l2e_idx, c->E, c->fixed, 2, nullptr, nullptr, diag, c->stream);
+  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 2, nullptr, nullptr, diag, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }
@@ -300,7 +354,7 @@ int tmop_gradient(tmop_ctx *c, const double *x, double *grad, tmop_det_status *d
   int g = 0;
   int rc = run(c, K_GRAD, a, &g);
   if (rc) return rc;
-  launch_e2l(c->dim, c->nn, c->NP, c->e_es, c->l2e_off, c->l2e_idx, c->E, c->fixed, 1, nullptr, nullptr, grad, c->stream);
+  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 1, nullptr, nullptr, grad, c->stream);
   launch_fin(g, nullptr, c->part_min, c->part_arg, 0.0, nullptr, 0.0, nullptr, det_out, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
@@ -424,7 +478,7 @@ int tmop_minres_step_op(tmop_ctx *c, const double *qdata, int64_t n, double *Av,
   a.qdata = qdata;
   int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
   if (rc) return rc;
-  launch_minres_step_op(c->dim, c->nn, c->NP, c->e_es, c->l2e_off, c->l2e_idx, c->E, c->fixed, n, Av, r1, r2, inv, z, v, w,
+  launch_minres_step_op(c->dim, c->nn, e2l_map(c), c->E, c->fixed, n, Av, r1, r2, inv, z, v, w,
                         w1buf, w2, x, rtol, st2 + (k & 1), st2 + ((k + 1) & 1), c->vpart1, c->vpart2, c->hist,
                         c->hist_cap, c->stream);
   CUDA_TRY(cudaGetLastError());

@@ -26,22 +26,95 @@ __device__ __forceinline__ const double *e_src(const double *E, uint32_t u, int 
   return E + ((((int64_t)(e >> es) * D * np + l) << es) | (int64_t)(e & ((1u << es) - 1u)));
 }
 
-template <int D>
-__global__ void e2l_kernel(int64_t nn, int np, int es, const int64_t *__restrict__ off, const uint32_t *__restrict__ idx,
-                           const double *__restrict__ E, const uint8_t *__restrict__ fixed, int mode,
-                           const double *__restrict__ v, const double *__restrict__ add, double *__restrict__ y) {
-  const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (node >= nn) return;
-  const int64_t b = off[node], end = off[node + 1];
-  double acc[D];
+// Copies of lattice node index i along one axis of a box with `ncell`
+// elements of order p: (element, local) pairs in ascending element order.
+struct LatAxis {
+  int e[2], l[2], n;
+};
+__device__ __forceinline__ void lat_axis(int i, int ncell, int p, LatAxis &o) {
+  const int q = i / p, r = i - q * p;
+  o.e[1] = o.l[1] = 0;
+  if (r != 0) {
+    o.n = 1; o.e[0] = q; o.l[0] = r;
+  } else if (q == 0) {
+    o.n = 1; o.e[0] = 0; o.l[0] = 0;
+  } else if (q == ncell) {
+    o.n = 1; o.e[0] = q - 1; o.l[0] = p;
+  } else {
+    o.n = 2; o.e[0] = q - 1; o.l[0] = p; o.e[1] = q; o.l[1] = 0;
+  }
+}
+
+// Sum of the E copies of `node` (all D components) in ascending element
+// order -- through the transpose map, or arithmetically on a lattice.
+template <int D, bool LAT>
+__device__ __forceinline__ void e2l_node(int64_t node, const E2LMap &m, const double *__restrict__ E,
+                                         double (&acc)[D]) {
 #pragma unroll
   for (int c = 0; c < D; ++c) acc[c] = 0.0;
-  for (int64_t k = b; k < end; ++k) {
-    int64_t cs;
-    const double *src = e_src(E, __ldg(idx + k), np, D, es, cs);
+  if constexpr (LAT) {
+    static_assert(D == 3, "lattice E->L is 3D");
+    const int p = m.lat_p, n1 = p + 1;
+    const uint32_t NX = (uint32_t)m.lat_n[0] * p + 1, NY = (uint32_t)m.lat_n[1] * p + 1;
+    const uint32_t nd = (uint32_t)node;
+    const uint32_t t = (uint32_t)(((uint64_t)nd * m.mag_x) >> m.sh_x);      // nd / NX
+    const uint32_t iz = (uint32_t)(((uint64_t)t * m.mag_y) >> m.sh_y);     // t / NY
+    const int ix = (int)(nd - t * NX), iy = (int)(t - iz * NY);
+    LatAxis ax, ay, az;
+    lat_axis(ix, m.lat_n[0], p, ax);
+    lat_axis(iy, m.lat_n[1], p, ay);
+    lat_axis((int)iz, m.lat_n[2], p, az);
+    const int64_t cs = (int64_t)m.np << m.es;
+    const uint32_t msk = (1u << m.es) - 1u;
+    // all (up to 8) copies' loads are issued before any is summed; the sum
+    // then runs in ascending element order (z, y, x lexicographic)
+    double val[8][D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) acc[c] += __ldg(src + c * cs);
+    for (int kz = 0; kz < 2; ++kz)
+#pragma unroll
+      for (int ky = 0; ky < 2; ++ky)
+#pragma unroll
+        for (int kx = 0; kx < 2; ++kx) {
+          const int k = (kz * 2 + ky) * 2 + kx;
+          if (kz < az.n && ky < ay.n && kx < ax.n) {
+            const uint32_t e = ax.e[kx] + (uint32_t)m.lat_n[0] * (ay.e[ky] + (uint32_t)m.lat_n[1] * az.e[kz]);
+            const int l = ax.l[kx] + n1 * (ay.l[ky] + n1 * az.l[kz]);
+            const double *src = E + (((((int64_t)(e >> m.es)) * D * m.np + l) << m.es) | (int64_t)(e & msk));
+#pragma unroll
+            for (int c = 0; c < D; ++c) val[k][c] = __ldg(src + c * cs);
+          }
+        }
+#pragma unroll
+    for (int kz = 0; kz < 2; ++kz)
+#pragma unroll
+      for (int ky = 0; ky < 2; ++ky)
+#pragma unroll
+        for (int kx = 0; kx < 2; ++kx) {
+          const int k = (kz * 2 + ky) * 2 + kx;
+          if (kz < az.n && ky < ay.n && kx < ax.n) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[c] += val[k][c];
+          }
+        }
+  } else {
+    const int64_t b = m.off[node], end = m.off[node + 1];
+    for (int64_t k = b; k < end; ++k) {
+      int64_t cs;
+      const double *src = e_src(E, __ldg(m.idx + k), m.np, D, m.es, cs);
+#pragma unroll
+      for (int c = 0; c < D; ++c) acc[c] += __ldg(src + c * cs);
+    }
   }
+}
+
+template <int D, bool LAT>
+__global__ void e2l_kernel(int64_t nn, const E2LMap m, const double *__restrict__ E, const uint8_t *__restrict__ fixed,
+                           int mode, const double *__restrict__ v, const double *__restrict__ add,
+                           double *__restrict__ y) {
+  const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= nn) return;
+  double acc[D];
+  e2l_node<D, LAT>(node, m, E, acc);
   const uint8_t f = __ldg(fixed + node);
 #pragma unroll
   for (int c = 0; c < D; ++c) {
@@ -53,15 +126,39 @@ __global__ void e2l_kernel(int64_t nn, int np, int es, const int64_t *__restrict
   }
 }
 
-int launch_e2l(int dim, int64_t nn, int np, int es, const int64_t *off, const uint32_t *idx, const double *E,
-               const uint8_t *fixed, int mode, const double *v, const double *add, double *y, cudaStream_t s) {
+int launch_e2l(int dim, int64_t nn, const E2LMap &m, const double *E, const uint8_t *fixed, int mode, const double *v,
+               const double *add, double *y, cudaStream_t s) {
   const int nt = 256;
   const int64_t grid = (nn + nt - 1) / nt;
   if (grid == 0) return 0;
   if (dim == 2)
-    e2l_kernel<2><<<(unsigned)grid, nt, 0, s>>>(nn, np, es, off, idx, E, fixed, mode, v, add, y);
+    e2l_kernel<2, false><<<(unsigned)grid, nt, 0, s>>>(nn, m, E, fixed, mode, v, add, y);
+  else if (m.lat_p > 0)
+    e2l_kernel<3, true><<<(unsigned)grid, nt, 0, s>>>(nn, m, E, fixed, mode, v, add, y);
   else
-    e2l_kernel<3><<<(unsigned)grid, nt, 0, s>>>(nn, np, es, off, idx, E, fixed, mode, v, add, y);
+    e2l_kernel<3, false><<<(unsigned)grid, nt, 0, s>>>(nn, m, E, fixed, mode, v, add, y);
+  return 0;
+}
+
+// Verifies that a restriction is the box lattice of build_box (mesh.py:118-164):
+// node(e, l) = sum_a (e_a p + l_a) stride_a.  Any mismatch sets *flag.
+__global__ void lattice_check_kernel(int64_t ne, int np, const int32_t *__restrict__ restr, int nx, int ny, int nz,
+                                     int p, int *flag) {
+  const int n1 = p + 1;
+  const int64_t NX = (int64_t)nx * p + 1, NY = (int64_t)ny * p + 1;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < ne * np; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = k / np;
+    const int l = (int)(k - e * np);
+    const int64_t ex = e % nx, ey = (e / nx) % ny, ez = e / ((int64_t)nx * ny);
+    const int lx = l % n1, ly = (l / n1) % n1, lz = l / (n1 * n1);
+    const int64_t want = (ex * p + lx) + NX * ((ey * p + ly) + NY * (ez * p + lz));
+    if (ez >= nz || (int64_t)__ldg(restr + k) != want) atomicOr(flag, 1);
+  }
+}
+
+int launch_lattice_check(int64_t ne, int np, const int32_t *restr, int nx, int ny, int nz, int p, int *flag,
+                         cudaStream_t s) {
+  lattice_check_kernel<<<148 * 8, 256, 0, s>>>(ne, np, restr, nx, ny, nz, p, flag);
   return 0;
 }
 
@@ -313,6 +410,9 @@ __global__ void __launch_bounds__(VEC_NT) minres_k1(int64_t n, double *__restric
 }
 
 // K2: alfa = sum(part1); Av -= (alfa/beta) r2; z = inv .* Av; partial beta2 = Av . z
+// V2: 16-byte vector accesses over element pairs (all pointers 16-byte
+// aligned; an odd tail element is taken by global thread 0).
+template <bool V2>
 __global__ void __launch_bounds__(VEC_NT) minres_k2(int64_t n, double *__restrict__ Av, const double *__restrict__ r2,
                                                     const double *__restrict__ inv, double *__restrict__ z,
                                                     const tmop_minres_state *cur, const double *__restrict__ part1,
@@ -322,18 +422,42 @@ __global__ void __launch_bounds__(VEC_NT) minres_k2(int64_t n, double *__restric
   const double alfa = reduce_partials(part1, np, sv);
   const double f = alfa / cur->beta;
   double s = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT) {
+  auto one = [&](int64_t i) {
     const double y = Av[i] - f * r2[i];
     Av[i] = y;
     const double zi = inv ? inv[i] * y : y;
     z[i] = zi;
     s += y * zi;
+  };
+  const int64_t gid = (int64_t)blockIdx.x * VEC_NT + threadIdx.x, stride = (int64_t)gridDim.x * VEC_NT;
+  if constexpr (V2) {
+    for (int64_t j = gid; j < (n >> 1); j += stride) {
+      const double2 a = reinterpret_cast<const double2 *>(Av)[j], r = reinterpret_cast<const double2 *>(r2)[j];
+      double2 y, zz;
+      y.x = a.x - f * r.x;
+      y.y = a.y - f * r.y;
+      reinterpret_cast<double2 *>(Av)[j] = y;
+      if (inv) {
+        const double2 iv = reinterpret_cast<const double2 *>(inv)[j];
+        zz.x = iv.x * y.x;
+        zz.y = iv.y * y.y;
+      } else {
+        zz = y;
+      }
+      reinterpret_cast<double2 *>(z)[j] = zz;
+      s += y.x * zz.x;
+      s += y.y * zz.y;
+    }
+    if (gid == 0 && (n & 1)) one(n - 1);
+  } else {
+    for (int64_t i = gid; i < n; i += stride) one(i);
   }
   s = block_sum<VEC_NT>(s, sv);
   if (threadIdx.x == 0) part2[blockIdx.x] = s;
 }
 
 // K3: beta2 = sum(part2); Givens recurrence; w_new (into w1buf); x += phi w_new; v = z / beta
+template <bool V2>
 __global__ void __launch_bounds__(VEC_NT) minres_k3(int64_t n, const double *__restrict__ z, double *__restrict__ v,
                                                     const double *__restrict__ w, double *__restrict__ w1buf,
                                                     const double *__restrict__ w2, double *__restrict__ x,
@@ -374,14 +498,34 @@ __global__ void __launch_bounds__(VEC_NT) minres_k3(int64_t n, const double *__r
   const double phi = s.cs * c.phibar;
   s.phibar = s.sn * c.phibar;
   s.relres = s.phibar / c.beta1;
-  const double rg = 1.0 / gamma;  // (v - oldeps w1 - delta w2) / gamma, solvers.py:158
-  (void)rg;
-  for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT) {
+  // w_new = (v - oldeps w1 - delta w2) / gamma (solvers.py:158), true divisions as the reference
+  auto one = [&](int64_t i) {
     const double vi = v[i];
     const double wn = (vi - oldeps * w2[i] - delta * w[i]) / gamma;
     w1buf[i] = wn;
     x[i] = x[i] + phi * wn;
     v[i] = z[i] / beta;
+  };
+  const int64_t gid = (int64_t)blockIdx.x * VEC_NT + threadIdx.x, stride = (int64_t)gridDim.x * VEC_NT;
+  if constexpr (V2) {
+    for (int64_t j = gid; j < (n >> 1); j += stride) {
+      const double2 vi = reinterpret_cast<const double2 *>(v)[j], a = reinterpret_cast<const double2 *>(w2)[j];
+      const double2 b = reinterpret_cast<const double2 *>(w)[j], xx = reinterpret_cast<const double2 *>(x)[j];
+      const double2 zz = reinterpret_cast<const double2 *>(z)[j];
+      double2 wn, xo, vo;
+      wn.x = (vi.x - oldeps * a.x - delta * b.x) / gamma;
+      wn.y = (vi.y - oldeps * a.y - delta * b.y) / gamma;
+      reinterpret_cast<double2 *>(w1buf)[j] = wn;
+      xo.x = xx.x + phi * wn.x;
+      xo.y = xx.y + phi * wn.y;
+      reinterpret_cast<double2 *>(x)[j] = xo;
+      vo.x = zz.x / beta;
+      vo.y = zz.y / beta;
+      reinterpret_cast<double2 *>(v)[j] = vo;
+    }
+    if (gid == 0 && (n & 1)) one(n - 1);
+  } else {
+    for (int64_t i = gid; i < n; i += stride) one(i);
   }
   if (beta == 0.0) {
     s.breakdown = 1;
@@ -402,14 +546,31 @@ void launch_minres_init(int64_t n, const double *b, const double *inv, double *x
   minres_init2_kernel<<<g, VEC_NT, 0, s>>>(n, z, v, part, g, st);
 }
 
+static bool al16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+static void launch_k23(int64_t n, double *Av, const double *r2, const double *inv, double *z, double *v,
+                       const double *w, double *w1buf, const double *w2, double *x, double rtol,
+                       tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, double *part2, double *hist,
+                       int hist_cap, int g, cudaStream_t s) {
+  const bool v2 = al16(Av) && al16(r2) && (!inv || al16(inv)) && al16(z) && al16(v) && al16(w) && al16(w1buf) &&
+                  al16(w2) && al16(x);
+  if (v2) {
+    minres_k2<true><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, part2, g);
+    minres_k3<true><<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol, hist, hist_cap);
+  } else {
+    minres_k2<false><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, part2, g);
+    minres_k3<false><<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol, hist,
+                                          hist_cap);
+  }
+}
+
 // Fused E->L gather + MINRES K1 for the TMOP operator (one pass over Av
 // instead of a gather write followed by a K1 read-modify-write):
 //   Av[i] = (fixed ? v : sum_E) ; Av -= (beta/oldb) r1 (itn >= 2) ; alfa partial v.Av
 // Grid = vec_grid(n), grid-stride over nodes, so the partial array has the
 // same length the following K2 / K3 expect.
-template <int D>
-__global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, int np, int es, const int64_t *__restrict__ off,
-                                                        const uint32_t *__restrict__ idx, const double *__restrict__ E,
+template <int D, bool LAT>
+__global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, const E2LMap m, const double *__restrict__ E,
                                                         const uint8_t *__restrict__ fixed, const double *__restrict__ v,
                                                         const double *__restrict__ r1, double *__restrict__ Av,
                                                         const tmop_minres_state *cur, double *__restrict__ part) {
@@ -420,14 +581,7 @@ __global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, int np, int 
   double s = 0.0;
   for (int64_t node = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; node < nn; node += (int64_t)gridDim.x * VEC_NT) {
     double acc[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) acc[c] = 0.0;
-    for (int64_t k = off[node]; k < off[node + 1]; ++k) {
-      int64_t cs;
-      const double *src = e_src(E, __ldg(idx + k), np, D, es, cs);
-#pragma unroll
-      for (int c = 0; c < D; ++c) acc[c] += __ldg(src + c * cs);
-    }
+    e2l_node<D, LAT>(node, m, E, acc);
     const uint8_t fl = __ldg(fixed + node);
 #pragma unroll
     for (int c = 0; c < D; ++c) {
@@ -443,18 +597,18 @@ __global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, int np, int 
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-void launch_minres_step_op(int dim, int64_t nn, int np, int es, const int64_t *off, const uint32_t *idx, const double *E,
-                           const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
+void launch_minres_step_op(int dim, int64_t nn, const E2LMap &m, const double *E, const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
                            const double *inv, double *z, double *v, const double *w, double *w1buf, const double *w2,
                            double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt, double *part1,
                            double *part2, double *hist, int hist_cap, cudaStream_t s) {
   const int g = vec_grid(n);
   if (dim == 2)
-    e2l_minres_k1<2><<<g, VEC_NT, 0, s>>>(nn, np, es, off, idx, E, fixed, v, r1, Av, cur, part1);
+    e2l_minres_k1<2, false><<<g, VEC_NT, 0, s>>>(nn, m, E, fixed, v, r1, Av, cur, part1);
+  else if (m.lat_p > 0)
+    e2l_minres_k1<3, true><<<g, VEC_NT, 0, s>>>(nn, m, E, fixed, v, r1, Av, cur, part1);
   else
-    e2l_minres_k1<3><<<g, VEC_NT, 0, s>>>(nn, np, es, off, idx, E, fixed, v, r1, Av, cur, part1);
-  minres_k2<<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, part2, g);
-  minres_k3<<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol, hist, hist_cap);
+    e2l_minres_k1<3, false><<<g, VEC_NT, 0, s>>>(nn, m, E, fixed, v, r1, Av, cur, part1);
+  launch_k23(n, Av, r2, inv, z, v, w, w1buf, w2, x, rtol, cur, nxt, part1, part2, hist, hist_cap, g, s);
 }
 
 void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r2, const double *inv, double *z,
@@ -463,8 +617,7 @@ void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r
                         double *hist, int hist_cap, cudaStream_t s) {
   const int g = vec_grid(n);
   minres_k1<<<g, VEC_NT, 0, s>>>(n, Av, r1, v, cur, part1);
-  minres_k2<<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, part2, g);
-  minres_k3<<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol, hist, hist_cap);
+  launch_k23(n, Av, r2, inv, z, v, w, w1buf, w2, x, rtol, cur, nxt, part1, part2, hist, hist_cap, g, s);
 }
 
 }  // namespace tmop

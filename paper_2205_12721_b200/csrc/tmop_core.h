@@ -13,8 +13,22 @@ constexpr int VEC_NT = 256;
 constexpr int VEC_GRID_CAP = 148 * 4;
 
 int vec_grid(int64_t n);
-int launch_e2l(int dim, int64_t nn, int np, int es, const int64_t *off, const uint32_t *idx, const double *E,
-               const uint8_t *fixed, int mode, const double *v, const double *add, double *y, cudaStream_t s);
+
+// Node-major view of the E-vector: the transposed restriction (CSR by node,
+// element-ascending) and the E layout; lat_p > 0 marks a verified
+// structured box lattice (lat_n element counts, order lat_p) whose copies
+// are enumerated arithmetically instead of through off / idx.
+struct E2LMap {
+  const int64_t *off;
+  const uint32_t *idx;
+  int np, es;
+  int lat_n[3], lat_p;
+  // exact division by the lattice node counts NX, NY for node ids < 2^31:
+  // q = (n * mag) >> sh  (host-computed, tmop_ctx_set_lattice)
+  uint64_t mag_x, mag_y;
+  int sh_x, sh_y;
+};
+int launch_e2l(int dim, int64_t nn, const E2LMap &m, const double *E, const uint8_t *fixed, int mode, const double *v, const double *add, double *y, cudaStream_t s);
 void launch_fin(int nparts, const double *psum, const double *pmin, const int64_t *parg, double sum_scale,
                 double *sum_out, double add_scale, const double *add, tmop_det_status *det_out, cudaStream_t s);
 int launch_metric_eval(int metric, int dim, int64_t n, const double *T, double *mu, double *P, double *H);
@@ -29,10 +43,12 @@ void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r
                         tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, double *part2,
                         double *hist, int hist_cap, cudaStream_t s);
 
-void launch_minres_step_op(int dim, int64_t nn, int np, int es, const int64_t *off, const uint32_t *idx, const double *E,
-                           const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
+void launch_minres_step_op(int dim, int64_t nn, const E2LMap &m, const double *E, const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
                            const double *inv, double *z, double *v, const double *w, double *w1buf, const double *w2,
                            double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt, double *part1,
                            double *part2, double *hist, int hist_cap, cudaStream_t s);
+
+int launch_lattice_check(int64_t ne, int np, const int32_t *restr, int nx, int ny, int nz, int p, int *flag,
+                         cudaStream_t s);
 
 }  // namespace tmop

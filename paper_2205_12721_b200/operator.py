@@ -9,6 +9,8 @@ implementation: without the library or a CUDA device every call raises.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -239,6 +241,13 @@ class TmopProblem:
             self.targets = build_targets(mesh, config.target, self.rule)
         _lib.check(self.lib.tmop_ctx_set_target(ctx, self.targets.inv_scale, self.targets.det_w),
                    "tmop_ctx_set_target")
+        # box lattices (build_box / Kershaw): verified on the device, then the
+        # E->L gathers enumerate node copies arithmetically
+        acc = _lib.C.c_int(0)
+        if d == 3 and getattr(mesh, "element_counts", None) is not None and os.environ.get("TMOP_LATTICE", "1") != "0":
+            nx, ny, nz = (int(c) for c in mesh.element_counts)
+            _lib.check(self.lib.tmop_ctx_set_lattice(ctx, nx, ny, nz, _lib.C.byref(acc)), "tmop_ctx_set_lattice")
+        self.lattice = bool(acc.value)
 
     def __del__(self):
         ctx = getattr(self, "_ctx", None)

@@ -277,3 +277,45 @@ def test_graph_replayed_minres_matches_eager(rng):
         assert e.iterations == gr.iterations
         assert torch.equal(e.x, gr.x)                  # same kernels, same order: bitwise
         assert e.rel_residual == gr.rel_residual
+
+
+@pytest.mark.parametrize("order,nq,counts", [(1, 3, (5, 4, 3)), (2, 4, (6, 3, 4)), (3, 5, (3, 2, 4)),
+                                             (4, 6, (2, 3, 2))])
+def test_lattice_gather_and_xline_kernels_match_generic(order, nq, counts, rng, monkeypatch):
+    """The structured-lattice E->L (tmop_ctx_set_lattice) sums the same copies
+    in the same order as the transpose map: bitwise equal results."""
+    import torch
+
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(3, counts, order)
+    cfg = P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT))
+    x = O.perturb(O.box_mesh(3, counts, order), rng, 0.2)
+    v = rng.standard_normal(x.shape)
+
+    def run():
+        p = P.TmopProblem(mesh, cfg, nq)
+        qd = p.hessian_setup(x)
+        out = (p.hessian_apply(qd, v), p.gradient(x), p.hessian_diagonal(qd), p.objective(x),
+               p.min_det_jacobian(x))
+        return p.lattice, out
+
+    lat, a = run()
+    assert lat
+    monkeypatch.setenv("TMOP_LATTICE", "0")
+    lat0, b = run()
+    assert not lat0
+    for u, w in zip(a[:3], b[:3]):
+        assert np.array_equal(u, w)
+    assert a[3] == b[3] and a[4] == b[4]
+    torch.cuda.synchronize()
+
+
+def test_lattice_rejects_non_lattice_restriction(rng):
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(3, (3, 3, 3), 2)
+    perm = mesh.restriction.copy()
+    perm[[0, 1]] = perm[[1, 0]]            # swap two elements: still a valid mesh, not the lattice order
+    from dataclasses import replace
+    m2 = replace(mesh, restriction=perm)
+    p = P.TmopProblem(m2, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), 4)
+    assert not p.lattice

@@ -18,6 +18,6 @@ ap.add_argument("--steps", type=int, default=10)
 a = ap.parse_args()
 nq = a.nq or a.order + 2
 r, _ = bench.run_order(a.order, a.n, nq, a.steps, 3, torch.device("cuda", 0))
-print(f"kernel={os.environ.get('TMOP_APPLY_KERNEL', 'col')} p={a.order} n={a.n} nq={nq} dofs={r['n_dofs']} "
+print(f"xl={os.environ.get('TMOP_XL', '1')} lattice={os.environ.get('TMOP_LATTICE', '1')} p={a.order} n={a.n} nq={nq} dofs={r['n_dofs']} "
       f"ms={r['ms_per_step']:.3f} elem_ms={r['t_elem_ms']:.3f} gather_ms={r['t_gather_ms']:.3f} "
       f"GDOF/s={r['gdofs']:.2f}")
