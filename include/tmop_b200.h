@@ -120,6 +120,17 @@ int tmop_hessian_apply(tmop_ctx *ctx, const double *qdata, const double *v,
 int tmop_hessian_apply_elements(tmop_ctx *ctx, const double *qdata,
                                 const double *v);
 int tmop_hessian_apply_gather(tmop_ctx *ctx, const double *v, double *y);
+
+/* Streaming pieces of the same action for host-resident pipelines
+ * (H2D of v / element kernel / E->L / D2H of y overlapped slab by slab):
+ * the element kernel over elements [e_begin, e_end) (e_begin % 8 == 0;
+ * reads v at those elements' nodes only), and the E->L sum + constraint
+ * fix-up for nodes [n_begin, n_end) (every element holding those nodes must
+ * have been processed).  Results are bitwise identical to
+ * tmop_hessian_apply. */
+int tmop_hessian_apply_elements_range(tmop_ctx *ctx, const double *qdata, const double *v, int64_t e_begin,
+                                      int64_t e_end);
+int tmop_hessian_apply_gather_range(tmop_ctx *ctx, const double *v, double *y, int64_t n_begin, int64_t n_end);
 /* AssembleGradDiagonalPA: hessian_diagonal (operator.py:420-459). */
 int tmop_hessian_diagonal(tmop_ctx *ctx, const double *qdata, double *diag);
 /* AddMultPA: gradient (operator.py:328-346). */

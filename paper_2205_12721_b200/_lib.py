@@ -45,6 +45,8 @@ _SIGS = {
     "tmop_ctx_set_stream": [_P, _P],
     "tmop_ctx_set_target": [_P, _D, _D],
     "tmop_ctx_set_lattice": [_P, _INT, _INT, _INT, _P],
+    "tmop_hessian_apply_elements_range": [_P, _P, _P, _I64, _I64],
+    "tmop_hessian_apply_gather_range": [_P, _P, _P, _I64, _I64],
     "tmop_qdata_fields": [_P],
     "tmop_qdata_stride": [_P],
     "tmop_qdata_size": [_P],

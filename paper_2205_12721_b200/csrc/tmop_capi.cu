@@ -329,6 +329,30 @@ int tmop_hessian_apply_elements(tmop_ctx *c, const double *qdata, const double *
   return run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
 }
 
+int tmop_hessian_apply_elements_range(tmop_ctx *c, const double *qdata, const double *v, int64_t e_begin,
+                                      int64_t e_end) {
+  if (!c || !qdata || !v) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (e_begin < 0 || e_end > c->ne || e_begin > e_end || (e_begin & 7))
+    return fail(TMOP_ERR_ARG, "element range [%lld, %lld) invalid (begin must be a multiple of 8, end <= %lld)",
+                (long long)e_begin, (long long)e_end, (long long)c->ne);
+  if (e_begin == e_end) return TMOP_OK;
+  ElemArgs a = base_args(c);
+  a.in = v;
+  a.qdata = qdata + e_begin * tmop_qdata_stride(c);
+  a.restr = c->restr + e_begin * c->NP;
+  a.E = c->E + e_begin * c->dim * c->NP;   // (element groups of 8 stay aligned: e_begin % 8 == 0)
+  a.ne = e_end - e_begin;
+  return run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
+}
+
+int tmop_hessian_apply_gather_range(tmop_ctx *c, const double *v, double *y, int64_t n_begin, int64_t n_end) {
+  if (!c || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (n_begin < 0 || n_end > c->nn || n_begin > n_end) return fail(TMOP_ERR_ARG, "node range invalid");
+  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 0, v, nullptr, y, c->stream, n_begin, n_end);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
 int tmop_hessian_apply_gather(tmop_ctx *c, const double *v, double *y) {
   if (!c || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
   launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 0, v, nullptr, y, c->stream);

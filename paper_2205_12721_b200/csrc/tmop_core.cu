@@ -108,11 +108,11 @@ __device__ __forceinline__ void e2l_node(int64_t node, const E2LMap &m, const do
 }
 
 template <int D, bool LAT>
-__global__ void e2l_kernel(int64_t nn, const E2LMap m, const double *__restrict__ E, const uint8_t *__restrict__ fixed,
-                           int mode, const double *__restrict__ v, const double *__restrict__ add,
-                           double *__restrict__ y) {
-  const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (node >= nn) return;
+__global__ void e2l_kernel(int64_t nn, int64_t n0, int64_t n1, const E2LMap m, const double *__restrict__ E,
+                           const uint8_t *__restrict__ fixed, int mode, const double *__restrict__ v,
+                           const double *__restrict__ add, double *__restrict__ y) {
+  const int64_t node = n0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= n1) return;
   double acc[D];
   e2l_node<D, LAT>(node, m, E, acc);
   const uint8_t f = __ldg(fixed + node);
@@ -127,16 +127,17 @@ __global__ void e2l_kernel(int64_t nn, const E2LMap m, const double *__restrict_
 }
 
 int launch_e2l(int dim, int64_t nn, const E2LMap &m, const double *E, const uint8_t *fixed, int mode, const double *v,
-               const double *add, double *y, cudaStream_t s) {
+               const double *add, double *y, cudaStream_t s, int64_t n0, int64_t n1) {
+  if (n1 < 0) n1 = nn;
   const int nt = 256;
-  const int64_t grid = (nn + nt - 1) / nt;
-  if (grid == 0) return 0;
+  const int64_t grid = (n1 - n0 + nt - 1) / nt;
+  if (grid <= 0) return 0;
   if (dim == 2)
-    e2l_kernel<2, false><<<(unsigned)grid, nt, 0, s>>>(nn, m, E, fixed, mode, v, add, y);
+    e2l_kernel<2, false><<<(unsigned)grid, nt, 0, s>>>(nn, n0, n1, m, E, fixed, mode, v, add, y);
   else if (m.lat_p > 0)
-    e2l_kernel<3, true><<<(unsigned)grid, nt, 0, s>>>(nn, m, E, fixed, mode, v, add, y);
+    e2l_kernel<3, true><<<(unsigned)grid, nt, 0, s>>>(nn, n0, n1, m, E, fixed, mode, v, add, y);
   else
-    e2l_kernel<3, false><<<(unsigned)grid, nt, 0, s>>>(nn, m, E, fixed, mode, v, add, y);
+    e2l_kernel<3, false><<<(unsigned)grid, nt, 0, s>>>(nn, n0, n1, m, E, fixed, mode, v, add, y);
   return 0;
 }
 

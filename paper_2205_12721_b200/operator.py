@@ -404,12 +404,88 @@ class TmopProblem:
         inputs are treated as zero, constrained outputs return v
         (operator.py:401-418)."""
         torch = _torch()
+        if (self.lattice and _is_torch(v) and not v.is_cuda and v.is_pinned() and v.dtype == torch.float64
+                and v.is_contiguous() and v.numel() == self.mesh.n_dofs
+                and (out is None or (not out.is_cuda and out.is_contiguous() and out.dtype == torch.float64))
+                and self.pipeline_slabs > 1):
+            return self._apply_host_pipelined(qdata, v, out)
         vt, host = self._in(v)
         y = self._dev_out(out, vt)
         _lib.check(self.lib.tmop_hessian_apply(self._ctx, _lib.ptr(qdata.data), _lib.ptr(vt), _lib.ptr(y)),
                    "tmop_hessian_apply")
         self._count("apply")
         return self._out(y, host, out)
+
+    # Host-resident Hessian action, pipelined slab by slab over z-layers of
+    # the box lattice: the H2D copy of slab k+1's new node planes, the element
+    # kernel + E->L of slab k and the D2H copy of the finished node planes of
+    # slab k-1 run on three streams (PCIe is full duplex), so the end-to-end
+    # time approaches max(H2D, D2H, compute) instead of their sum.  Bitwise
+    # identical to the one-shot apply.
+    pipeline_slabs = int(os.environ.get("TMOP_PIPE_SLABS", "8"))
+
+    def _apply_host_pipelined(self, qdata: HessQData, vh, out):
+        torch = _torch()
+        m = self.mesh
+        nx, ny, nz = m.element_counts
+        p = m.order
+        NX, NY = nx * p + 1, ny * p + 1
+        nn, ne, layer = m.n_nodes, m.n_elements, nx * ny
+        if out is None:
+            out = torch.empty(m.n_dofs, dtype=torch.float64, pin_memory=True)
+        pipe = getattr(self, "_pipe", None)
+        if pipe is None:
+            pipe = self._pipe = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device),
+                                 torch.cuda.Stream(self.device))
+        h2d, comp, d2h = pipe
+        caller = torch.cuda.current_stream(self.device)
+        vt = torch.empty(m.n_dofs, dtype=torch.float64, device=self.device)
+        y = torch.empty_like(vt)
+        V, Y, VH, OH = vt.view(3, nn), y.view(3, nn), vh.view(3, nn), out.view(3, nn)
+        for s_ in pipe:
+            s_.wait_stream(caller)
+
+        def node_lo(e):
+            ex, ey, ez = e % nx, (e // nx) % ny, e // layer
+            return ex * p + NX * (ey * p + NY * ez * p)
+
+        def node_hi(e):   # last node of element e, + 1
+            ex, ey, ez = e % nx, (e // nx) % ny, e // layer
+            return (ex * p + p) + NX * ((ey * p + p) + NY * (ez * p + p)) + 1
+
+        ns = min(self.pipeline_slabs, nz)
+        bounds = [((k * nz) // ns) * layer // 8 * 8 for k in range(ns)] + [ne]
+        copied, done = 0, 0
+        for k in range(ns):
+            e0, e1 = bounds[k], bounds[k + 1]
+            if e1 <= e0:
+                continue
+            hi = node_hi(e1 - 1)
+            with torch.cuda.stream(h2d):
+                if hi > copied:
+                    for c in range(3):
+                        V[c, copied:hi].copy_(VH[c, copied:hi], non_blocking=True)
+                    copied = hi
+            comp.wait_stream(h2d)
+            fin = nn if e1 == ne else (e1 // layer) * p * NX * NY
+            with torch.cuda.stream(comp):
+                self._sync_stream()
+                _lib.check(self.lib.tmop_hessian_apply_elements_range(
+                    self._ctx, _lib.ptr(qdata.data), _lib.ptr(vt), e0, e1), "tmop_hessian_apply_elements_range")
+                if fin > done:
+                    _lib.check(self.lib.tmop_hessian_apply_gather_range(
+                        self._ctx, _lib.ptr(vt), _lib.ptr(y), done, fin), "tmop_hessian_apply_gather_range")
+            d2h.wait_stream(comp)
+            if fin > done:
+                with torch.cuda.stream(d2h):
+                    for c in range(3):
+                        OH[c, done:fin].copy_(Y[c, done:fin], non_blocking=True)
+                done = fin
+        d2h.synchronize()
+        vt.record_stream(comp)
+        y.record_stream(d2h)
+        self._count("apply")
+        return out
 
     def hessian_diagonal(self, qdata: HessQData, out=None):
         torch = _torch()

@@ -319,3 +319,26 @@ def test_lattice_rejects_non_lattice_restriction(rng):
     m2 = replace(mesh, restriction=perm)
     p = P.TmopProblem(m2, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), 4)
     assert not p.lattice
+
+
+@pytest.mark.parametrize("order,nq,counts,slabs", [(2, 4, (6, 5, 9), 4), (1, 3, (7, 3, 5), 8), (3, 5, (3, 4, 5), 3)])
+def test_pipelined_host_apply_is_bitwise_equal(order, nq, counts, slabs, rng, monkeypatch):
+    """Pinned host input: the slab-pipelined H2D / element kernel / E->L / D2H
+    path returns exactly the one-shot device result."""
+    import torch
+
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(3, counts, order)
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), nq)
+    p.pipeline_slabs = slabs
+    x = O.perturb(O.box_mesh(3, counts, order), rng, 0.2)
+    qd = p.hessian_setup(x)
+    v = torch.from_numpy(rng.standard_normal(mesh.n_dofs))
+    ref = p.hessian_apply(qd, v.cuda()).cpu()
+    vh = v.pin_memory()
+    out = torch.empty(mesh.n_dofs, dtype=torch.float64, pin_memory=True)
+    got = p.hessian_apply(qd, vh, out=out)
+    assert got.data_ptr() == out.data_ptr()
+    assert torch.equal(got, ref)
+    got2 = p.hessian_apply(qd, vh)
+    assert torch.equal(got2, ref)
