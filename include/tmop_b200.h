@@ -98,10 +98,20 @@ int tmop_qdata_reference_fields(const tmop_ctx *ctx);
 int tmop_qdata_to_reference(tmop_ctx *ctx, const double *qdata, double *out);
 /* Configure the displacement-limiting term (operator.py:57-76, 463-533):
  * x0 (reference positions, T-vector) and delta_nodal (n_nodes, or NULL for
- * the scalar delta) are DEVICE pointers; weight > 0 enables, 0 disables. */
+ * the scalar delta) are DEVICE pointers kept by reference; x0 == NULL
+ * disables the term.  When enabled, objective / gradient / hessian_apply /
+ * hessian_diagonal / minres_step_op include it exactly where the reference
+ * adds it (operator.py:324-325, 343-344, 415-416, 452-457). */
 int tmop_ctx_set_limiting(tmop_ctx *ctx, const double *x0,
                           const double *delta_nodal, double delta,
                           double weight);
+/* The limiting term alone (operator.py:488-533): value into *out (device
+ * scalar), raw gradient B^T(c (B(x - x0))) and raw action B^T(c B v) (no
+ * constraint handling), as limiting_value / limiting_gradient /
+ * limiting_hessian_apply. */
+int tmop_limiting_value(tmop_ctx *ctx, const double *x, double *out);
+int tmop_limiting_gradient(tmop_ctx *ctx, const double *x, double *y);
+int tmop_limiting_apply(tmop_ctx *ctx, const double *v, double *y);
 const char *tmop_last_error(void);
 
 /* ---- operator entry points (all async on the context stream) ---------- */

@@ -237,9 +237,9 @@ class Discretization:
         return [self.G if k == direction else self.B for k in range(self.d)]
 
     def gather(self, vec2):
-        """(d, N) -> (d, Ne, n,..,n)."""
+        """(c, N) -> (c, Ne, n,..,n) for any number c of fields (fe:180-187)."""
         e = vec2[:, self.mesh.restriction]
-        return e.reshape((self.d, self.mesh.n_elements) + (self.n,) * self.d)
+        return e.reshape((vec2.shape[0], self.mesh.n_elements) + (self.n,) * self.d)
 
     def scatter(self, E):
         """(d, Ne, n^d) E-vector -> (d, N), ascending element order (fe:189-204)."""

@@ -53,6 +53,9 @@ _SIGS = {
     "tmop_qdata_reference_fields": [_P],
     "tmop_qdata_to_reference": [_P, _P, _P],
     "tmop_ctx_set_limiting": [_P, _P, _P, _D, _D],
+    "tmop_limiting_value": [_P, _P, _P],
+    "tmop_limiting_gradient": [_P, _P, _P],
+    "tmop_limiting_apply": [_P, _P, _P],
     "tmop_hessian_setup": [_P, _P, _P, _P],
     "tmop_hessian_apply": [_P, _P, _P, _P],
     "tmop_hessian_apply_elements": [_P, _P, _P],

@@ -55,6 +55,11 @@ struct tmop_ctx {
   uint64_t mag_x, mag_y;
   int sh_x, sh_y;
   int *flag;             // device scratch word
+  // displacement limiting (tmop_ctx_set_limiting); buffers allocated on first use
+  int lim_on;
+  const double *lim_x0, *lim_dn;
+  double lim_delta, lim_weight;
+  double *E2, *lim_y, *lim_val;
   double *hist;      // MINRES residual history (device, optional)
   int hist_cap;
 };
@@ -134,6 +139,44 @@ static int run(tmop_ctx *c, int kind, ElemArgs &a, int *grid_out) {
   return TMOP_OK;
 }
 
+// Limiting term node sums into c->lim_y (raw, no constraint fix-up): kind
+// K_LIM_FIELD on `in` (minus x0 when given, constrained components zeroed
+// when mask) or K_LIM_DIAG; E2 -> e2l mode 3.
+static int lim_nodes(tmop_ctx *c, int kind, const double *in, const double *x0, int mask) {
+  ElemArgs a = base_args(c);
+  a.in = in;
+  a.E = c->E2;
+  a.lim_x0 = x0;
+  a.lim_dn = c->lim_dn;
+  a.lim_delta = c->lim_delta;
+  a.lim_base = 2.0 * c->lim_weight * c->det_w;
+  a.lim_mask = mask;
+  const int g = launch_elem(c->dim, c->n1, c->nq, kind, a, c->tab, c->stream);
+  if (g < 0) return fail(TMOP_ERR_ARG, "no limiting kernel for dim=%d p=%d n_q=%d", c->dim, c->order, c->nq);
+  CUDA_TRY(cudaGetLastError());
+  E2LMap m = e2l_map(c);
+  m.es = 0;
+  launch_e2l(c->dim, c->nn, m, c->E2, c->fixed, 3, nullptr, nullptr, c->lim_y, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+// Limiting value 1/2 sum c_q |B (x - x0)|^2 into c->lim_val (device).
+static int lim_value(tmop_ctx *c, const double *x) {
+  ElemArgs a = base_args(c);
+  a.in = x;
+  a.lim_x0 = c->lim_x0;
+  a.lim_dn = c->lim_dn;
+  a.lim_delta = c->lim_delta;
+  a.lim_base = 2.0 * c->lim_weight * c->det_w;
+  const int g = launch_elem(c->dim, c->n1, c->nq, K_LIM_VALUE, a, c->tab, c->stream);
+  if (g < 0) return fail(TMOP_ERR_ARG, "no limiting kernel for dim=%d p=%d n_q=%d", c->dim, c->order, c->nq);
+  CUDA_TRY(cudaGetLastError());
+  launch_fin(g, c->part_sum, nullptr, nullptr, 0.5, c->lim_val, 0.0, nullptr, nullptr, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
 extern "C" {
 
 const char *tmop_last_error(void) { return g_err; }
@@ -205,6 +248,9 @@ int tmop_ctx_destroy(tmop_ctx *c) {
   cudaFree(c->vpart1);
   cudaFree(c->vpart2);
   cudaFree(c->flag);
+  cudaFree(c->E2);
+  cudaFree(c->lim_y);
+  cudaFree(c->lim_val);
   delete c;
   return TMOP_OK;
 }
@@ -291,9 +337,55 @@ int tmop_qdata_to_reference(tmop_ctx *c, const double *qdata, double *out) {
   return TMOP_OK;
 }
 
-int tmop_ctx_set_limiting(tmop_ctx *c, const double *, const double *, double, double) {
+int tmop_ctx_set_limiting(tmop_ctx *c, const double *x0, const double *delta_nodal, double delta, double weight) {
   if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
-  return fail(TMOP_ERR_ARG, "limiting term not available in this build");
+  if (!x0) {
+    c->lim_on = 0;
+    return TMOP_OK;
+  }
+  if (!(weight > 0.0)) return fail(TMOP_ERR_ARG, "limiting weight must be positive");
+  if (!delta_nodal && !(delta > 0.0)) return fail(TMOP_ERR_ARG, "limiting delta must be positive");
+  if (!c->E2) {
+    const size_t esz = (size_t)(c->ne > 0 ? c->ne : 1) * c->dim * c->NP;
+    CUDA_TRY(cudaMalloc(&c->E2, esz * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&c->lim_y, (size_t)(c->nn > 0 ? c->nn : 1) * c->dim * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&c->lim_val, sizeof(double)));
+  }
+  c->lim_on = 1;
+  c->lim_x0 = x0;
+  c->lim_dn = delta_nodal;
+  c->lim_delta = delta;
+  c->lim_weight = weight;
+  return TMOP_OK;
+}
+
+int tmop_limiting_value(tmop_ctx *c, const double *x, double *out) {
+  if (!c || !x || !out) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (!c->lim_on) return fail(TMOP_ERR_ARG, "limiting term not configured (tmop_ctx_set_limiting)");
+  int rc = lim_value(c, x);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out, c->lim_val, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  return TMOP_OK;
+}
+
+int tmop_limiting_gradient(tmop_ctx *c, const double *x, double *y) {
+  if (!c || !x || !y) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (!c->lim_on) return fail(TMOP_ERR_ARG, "limiting term not configured (tmop_ctx_set_limiting)");
+  int rc = lim_nodes(c, K_LIM_FIELD, x, c->lim_x0, 0);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(y, c->lim_y, (size_t)c->nn * c->dim * sizeof(double), cudaMemcpyDeviceToDevice,
+                           c->stream));
+  return TMOP_OK;
+}
+
+int tmop_limiting_apply(tmop_ctx *c, const double *v, double *y) {
+  if (!c || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (!c->lim_on) return fail(TMOP_ERR_ARG, "limiting term not configured (tmop_ctx_set_limiting)");
+  int rc = lim_nodes(c, K_LIM_FIELD, v, nullptr, 0);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(y, c->lim_y, (size_t)c->nn * c->dim * sizeof(double), cudaMemcpyDeviceToDevice,
+                           c->stream));
+  return TMOP_OK;
 }
 
 int tmop_hessian_setup(tmop_ctx *c, const double *x, double *qdata, tmop_det_status *det_out) {
@@ -311,14 +403,9 @@ int tmop_hessian_setup(tmop_ctx *c, const double *x, double *qdata, tmop_det_sta
 
 int tmop_hessian_apply(tmop_ctx *c, const double *qdata, const double *v, double *y) {
   if (!c || !qdata || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
-  ElemArgs a = base_args(c);
-  a.in = v;
-  a.qdata = qdata;
-  int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
+  int rc = tmop_hessian_apply_elements(c, qdata, v);
   if (rc) return rc;
-  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 0, v, nullptr, y, c->stream);
-  CUDA_TRY(cudaGetLastError());
-  return TMOP_OK;
+  return tmop_hessian_apply_gather(c, v, y);
 }
 
 int tmop_hessian_apply_elements(tmop_ctx *c, const double *qdata, const double *v) {
@@ -326,12 +413,16 @@ int tmop_hessian_apply_elements(tmop_ctx *c, const double *qdata, const double *
   ElemArgs a = base_args(c);
   a.in = v;
   a.qdata = qdata;
-  return run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
+  int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
+  if (rc) return rc;
+  // limiting part of the action on the masked input (operator.py:415-416)
+  return c->lim_on ? lim_nodes(c, K_LIM_FIELD, v, nullptr, 1) : TMOP_OK;
 }
 
 int tmop_hessian_apply_elements_range(tmop_ctx *c, const double *qdata, const double *v, int64_t e_begin,
                                       int64_t e_end) {
   if (!c || !qdata || !v) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (c->lim_on) return fail(TMOP_ERR_ARG, "range apply does not support the limiting term");
   if (e_begin < 0 || e_end > c->ne || e_begin > e_end || (e_begin & 7))
     return fail(TMOP_ERR_ARG, "element range [%lld, %lld) invalid (begin must be a multiple of 8, end <= %lld)",
                 (long long)e_begin, (long long)e_end, (long long)c->ne);
@@ -355,7 +446,7 @@ int tmop_hessian_apply_gather_range(tmop_ctx *c, const double *v, double *y, int
 
 int tmop_hessian_apply_gather(tmop_ctx *c, const double *v, double *y) {
   if (!c || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
-  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 0, v, nullptr, y, c->stream);
+  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 0, v, c->lim_on ? c->lim_y : nullptr, y, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }
@@ -366,7 +457,11 @@ int tmop_hessian_diagonal(tmop_ctx *c, const double *qdata, double *diag) {
   a.qdata = qdata;
   int rc = run(c, metric_is_template(c->metric) ? K_DIAG : K_DIAG_NT, a, nullptr);
   if (rc) return rc;
-  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 2, nullptr, nullptr, diag, c->stream);
+  if (c->lim_on) {   // (B.B)^T c_q added to every component (operator.py:452-457)
+    rc = lim_nodes(c, K_LIM_DIAG, nullptr, nullptr, 0);
+    if (rc) return rc;
+  }
+  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 2, nullptr, c->lim_on ? c->lim_y : nullptr, diag, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }
@@ -378,7 +473,11 @@ int tmop_gradient(tmop_ctx *c, const double *x, double *grad, tmop_det_status *d
   int g = 0;
   int rc = run(c, K_GRAD, a, &g);
   if (rc) return rc;
-  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 1, nullptr, nullptr, grad, c->stream);
+  if (c->lim_on) {   // operator.py:343-344
+    rc = lim_nodes(c, K_LIM_FIELD, x, c->lim_x0, 0);
+    if (rc) return rc;
+  }
+  launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 1, nullptr, c->lim_on ? c->lim_y : nullptr, grad, c->stream);
   launch_fin(g, nullptr, c->part_min, c->part_arg, 0.0, nullptr, 0.0, nullptr, det_out, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
@@ -389,9 +488,14 @@ int tmop_objective(tmop_ctx *c, const double *x, double *energy_out, tmop_det_st
   ElemArgs a = base_args(c);
   a.in = x;
   int g = 0;
+  if (c->lim_on) {   // operator.py:324-325 (added after the metric sum)
+    int rc0 = lim_value(c, x);
+    if (rc0) return rc0;
+  }
   int rc = run(c, K_ENERGY, a, &g);
   if (rc) return rc;
-  launch_fin(g, c->part_sum, c->part_min, c->part_arg, a.coef_e, energy_out, 0.0, nullptr, det_out, c->stream);
+  launch_fin(g, c->part_sum, c->part_min, c->part_arg, a.coef_e, energy_out, 1.0, c->lim_on ? c->lim_val : nullptr,
+             det_out, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }
@@ -502,7 +606,12 @@ int tmop_minres_step_op(tmop_ctx *c, const double *qdata, int64_t n, double *Av,
   a.qdata = qdata;
   int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
   if (rc) return rc;
-  launch_minres_step_op(c->dim, c->nn, e2l_map(c), c->E, c->fixed, n, Av, r1, r2, inv, z, v, w,
+  if (c->lim_on) {
+    rc = lim_nodes(c, K_LIM_FIELD, v, nullptr, 1);
+    if (rc) return rc;
+  }
+  launch_minres_step_op(c->dim, c->nn, e2l_map(c), c->E, c->lim_on ? c->lim_y : nullptr, c->fixed, n, Av, r1, r2,
+                        inv, z, v, w,
                         w1buf, w2, x, rtol, st2 + (k & 1), st2 + ((k + 1) & 1), c->vpart1, c->vpart2, c->hist,
                         c->hist_cap, c->stream);
   CUDA_TRY(cudaGetLastError());

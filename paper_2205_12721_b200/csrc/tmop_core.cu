@@ -15,7 +15,8 @@ namespace tmop {
 // y[c][node] = sum over the node's element copies, ascending element order
 // (np.add.at order, fe.py:189-204).  mode: 0 = apply (constrained entries
 // copy v, operator.py:417), 1 = gradient (constrained -> 0, operator.py:345),
-// 2 = diagonal (constrained -> 1, operator.py:458).  `add` (may be NULL) is
+// 2 = diagonal (constrained -> 1, operator.py:458), 3 = raw sums (no fix-up;
+// the limiting term's node sums).  `add` (may be NULL) is
 // an extra T-vector added before the constraint fix-up (limiting term).
 // E layout: element groups of 2^es elements interleaved (element fastest):
 // E[((e >> es) * D * np + c * np + l) << es | (e & (2^es - 1))]; es = 0 is
@@ -121,7 +122,7 @@ __global__ void e2l_kernel(int64_t nn, int64_t n0, int64_t n1, const E2LMap m, c
     const int64_t i = c * nn + node;
     double r = acc[c];
     if (add) r += add[i];
-    if ((f >> c) & 1) r = (mode == 0) ? v[i] : (mode == 1 ? 0.0 : 1.0);
+    if (mode != 3 && ((f >> c) & 1)) r = (mode == 0) ? v[i] : (mode == 1 ? 0.0 : 1.0);
     y[i] = r;
   }
 }
@@ -572,6 +573,7 @@ static void launch_k23(int64_t n, double *Av, const double *r2, const double *in
 // same length the following K2 / K3 expect.
 template <int D, bool LAT>
 __global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, const E2LMap m, const double *__restrict__ E,
+                                                        const double *__restrict__ add,
                                                         const uint8_t *__restrict__ fixed, const double *__restrict__ v,
                                                         const double *__restrict__ r1, double *__restrict__ Av,
                                                         const tmop_minres_state *cur, double *__restrict__ part) {
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, const E2LMap
     for (int c = 0; c < D; ++c) {
       const int64_t i = c * nn + node;
       const double vi = v[i];
-      double y = ((fl >> c) & 1) ? vi : acc[c];
+      double y = ((fl >> c) & 1) ? vi : (add ? acc[c] + add[i] : acc[c]);
       if (sub) y = y - f * r1[i];
       Av[i] = y;
       s += vi * y;
@@ -598,17 +600,18 @@ __global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, const E2LMap
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-void launch_minres_step_op(int dim, int64_t nn, const E2LMap &m, const double *E, const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
+void launch_minres_step_op(int dim, int64_t nn, const E2LMap &m, const double *E, const double *add,
+                           const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
                            const double *inv, double *z, double *v, const double *w, double *w1buf, const double *w2,
                            double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt, double *part1,
                            double *part2, double *hist, int hist_cap, cudaStream_t s) {
   const int g = vec_grid(n);
   if (dim == 2)
-    e2l_minres_k1<2, false><<<g, VEC_NT, 0, s>>>(nn, m, E, fixed, v, r1, Av, cur, part1);
+    e2l_minres_k1<2, false><<<g, VEC_NT, 0, s>>>(nn, m, E, add, fixed, v, r1, Av, cur, part1);
   else if (m.lat_p > 0)
-    e2l_minres_k1<3, true><<<g, VEC_NT, 0, s>>>(nn, m, E, fixed, v, r1, Av, cur, part1);
+    e2l_minres_k1<3, true><<<g, VEC_NT, 0, s>>>(nn, m, E, add, fixed, v, r1, Av, cur, part1);
   else
-    e2l_minres_k1<3, false><<<g, VEC_NT, 0, s>>>(nn, m, E, fixed, v, r1, Av, cur, part1);
+    e2l_minres_k1<3, false><<<g, VEC_NT, 0, s>>>(nn, m, E, add, fixed, v, r1, Av, cur, part1);
   launch_k23(n, Av, r2, inv, z, v, w, w1buf, w2, x, rtol, cur, nxt, part1, part2, hist, hist_cap, g, s);
 }
 

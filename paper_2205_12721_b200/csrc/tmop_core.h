@@ -45,7 +45,8 @@ void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r
                         tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, double *part2,
                         double *hist, int hist_cap, cudaStream_t s);
 
-void launch_minres_step_op(int dim, int64_t nn, const E2LMap &m, const double *E, const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
+void launch_minres_step_op(int dim, int64_t nn, const E2LMap &m, const double *E, const double *add,
+                           const uint8_t *fixed, int64_t n, double *Av, const double *r1, const double *r2,
                            const double *inv, double *z, double *v, const double *w, double *w1buf, const double *w2,
                            double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt, double *part1,
                            double *part2, double *hist, int hist_cap, cudaStream_t s);

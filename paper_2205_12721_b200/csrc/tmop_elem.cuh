@@ -37,7 +37,10 @@ enum Kind : int {
   K_DIAG = 7,     // hessian_diagonal     (operator.py:420-459)
   K_APPLY_NT = 8, // hessian_apply, non-template metrics (mu_302 / mu_321)
   K_DIAG_NT = 9,  // hessian_diagonal, non-template metrics
-  K_COUNT = 10
+  K_LIM_VALUE = 10,  // limiting_value        (operator.py:488-495)
+  K_LIM_FIELD = 11,  // limiting gradient / Hessian action (operator.py:497-533)
+  K_LIM_DIAG = 12,   // limiting part of hessian_diagonal (operator.py:452-457)
+  K_COUNT = 13
 };
 
 // Tuning knobs (compile-time overrides for tools/build_variant.sh; 0 = the
@@ -141,6 +144,12 @@ struct ElemArgs {
   double coef_e;      // omega * det_w               (operator.py:314)
   double coef_g;      // omega * det_w * inv_s       (operator.py:330)
   double coef_h;      // omega * det_w * inv_s^2     (operator.py:358-359)
+  // limiting term (tmop_lim.cuh)
+  const double *__restrict__ lim_x0;   // reference positions subtracted from `in` (NULL: none)
+  const double *__restrict__ lim_dn;   // nodal delta (NULL: scalar lim_delta)
+  double lim_delta;
+  double lim_base;    // 2 * weight * det_w  (operator.py:477)
+  int lim_mask;       // zero constrained input components (hessian_apply)
 };
 
 // Point slot of quadrature point q (x fastest, fe.py:134-140) inside a lean

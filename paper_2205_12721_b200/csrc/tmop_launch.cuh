@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "tmop_lim.cuh"
 #include "tmop_xl.cuh"
 #include "tmop_diag.cuh"
 #include "tmop_elem.cuh"
@@ -81,9 +82,28 @@ int launch_diag(ElemArgs &a, const Tab &t, cudaStream_t s) {
 }
 
 template <int DIM, int N, int Q, int KIND>
+int launch_lim(ElemArgs &a, const Tab &t, cudaStream_t s) {
+  using LC = LimCfg<DIM, N, Q>;
+  a.ngroups = (a.ne + LC::EPB - 1) / LC::EPB;
+  a.e_es = 0;
+  const int grid = (int)std::min<int64_t>(a.ngroups, GRID_CAP);
+  if (grid == 0) return 0;
+  auto kfn = lim_kernel<DIM, N, Q, KIND>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, LC::SMEM) != cudaSuccess) return -2;
+    configured = true;
+  }
+  kfn<<<grid, LC::NT, LC::SMEM, s>>>(a, t);
+  return grid;
+}
+
+template <int DIM, int N, int Q, int KIND>
 int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
   using CF = Cfg<DIM, N, Q>;
-  if constexpr (KIND == K_DIAG || KIND == K_DIAG_NT) {
+  if constexpr (KIND == K_LIM_VALUE || KIND == K_LIM_FIELD || KIND == K_LIM_DIAG) {
+    return launch_lim<DIM, N, Q, KIND>(a, t, s);
+  } else if constexpr (KIND == K_DIAG || KIND == K_DIAG_NT) {
     return launch_diag<DIM, N, Q, KIND == K_DIAG_NT>(a, t, s);
   } else {
     if constexpr (DIM == 3 && xl_kind<N, KIND>() && xl_supported<N, Q>()) {
@@ -117,6 +137,9 @@ int launch_kind(int kind, ElemArgs &a, const Tab &t, cudaStream_t s) {
     case K_DIAG: return launch_one<DIM, N, Q, K_DIAG>(a, t, s);
     case K_APPLY_NT: return launch_one<DIM, N, Q, K_APPLY_NT>(a, t, s);
     case K_DIAG_NT: return launch_one<DIM, N, Q, K_DIAG_NT>(a, t, s);
+    case K_LIM_VALUE: return launch_one<DIM, N, Q, K_LIM_VALUE>(a, t, s);
+    case K_LIM_FIELD: return launch_one<DIM, N, Q, K_LIM_FIELD>(a, t, s);
+    case K_LIM_DIAG: return launch_one<DIM, N, Q, K_LIM_DIAG>(a, t, s);
     default: return -1;
   }
 }

@@ -212,7 +212,6 @@ class TmopProblem:
         self.batch_elements = max(1, batch_quad_points // self.n_quad_total)
         if config.limiting is not None:
             config.limiting.validate(mesh.n_dofs)
-            raise NotImplementedError("the displacement-limiting term is not built yet on the device path")
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.dmesh = DeviceMesh(mesh, self.device)
         self._stream = None
@@ -241,6 +240,20 @@ class TmopProblem:
             self.targets = build_targets(mesh, config.target, self.rule)
         _lib.check(self.lib.tmop_ctx_set_target(ctx, self.targets.inv_scale, self.targets.det_w),
                    "tmop_ctx_set_target")
+        self._lim = None
+        if config.limiting is not None:
+            # device copies owned here; the context keeps the pointers (operator.py:463-486)
+            lim = config.limiting
+            x0 = torch.from_numpy(np.ascontiguousarray(lim.reference, dtype=np.float64)).to(self.device)
+            dn = None
+            if np.ndim(lim.delta) != 0:
+                dn = torch.from_numpy(np.ascontiguousarray(lim.delta, dtype=np.float64).reshape(-1)).to(self.device)
+                if dn.numel() != mesh.n_nodes:
+                    raise ValueError(f"nodal limiting delta needs {mesh.n_nodes} values, got {dn.numel()}")
+            self._lim = (x0, dn)
+            _lib.check(self.lib.tmop_ctx_set_limiting(
+                ctx, _lib.ptr(x0), _lib.ptr(dn) if dn is not None else None,
+                float(lim.delta) if dn is None else 0.0, float(lim.weight)), "tmop_ctx_set_limiting")
         # box lattices (build_box / Kershaw): verified on the device, then the
         # E->L gathers enumerate node copies arithmetically
         acc = _lib.C.c_int(0)
@@ -407,7 +420,7 @@ class TmopProblem:
         if (self.lattice and _is_torch(v) and not v.is_cuda and v.is_pinned() and v.dtype == torch.float64
                 and v.is_contiguous() and v.numel() == self.mesh.n_dofs
                 and (out is None or (not out.is_cuda and out.is_contiguous() and out.dtype == torch.float64))
-                and self.pipeline_slabs > 1):
+                and self.pipeline_slabs > 1 and self._lim is None):
             return self._apply_host_pipelined(qdata, v, out)
         vt, host = self._in(v)
         y = self._dev_out(out, vt)
@@ -494,6 +507,34 @@ class TmopProblem:
         _lib.check(self.lib.tmop_hessian_diagonal(self._ctx, _lib.ptr(qdata.data), _lib.ptr(y)),
                    "tmop_hessian_diagonal")
         return self._out(y, qdata.host)
+
+    # ------------------------------------------------ limiting term alone
+    def _need_lim(self):
+        if self._lim is None:
+            raise ValueError("the objective has no limiting term (ObjectiveConfig.limiting is None)")
+
+    def limiting_value(self, x) -> float:
+        """1/2 sum_q c_q |B(x - x0)|^2 (operator.py:488-495)."""
+        self._need_lim()
+        xt, _ = self._in(x)
+        _lib.check(self.lib.tmop_limiting_value(self._ctx, _lib.ptr(xt), _lib.ptr(self._scalar)), "tmop_limiting_value")
+        return float(self._scalar.item())
+
+    def limiting_gradient(self, x):
+        """B^T (c_q B(x - x0)), no constraint handling (operator.py:497-512)."""
+        self._need_lim()
+        xt, host = self._in(x)
+        y = _torch().empty_like(xt)
+        _lib.check(self.lib.tmop_limiting_gradient(self._ctx, _lib.ptr(xt), _lib.ptr(y)), "tmop_limiting_gradient")
+        return self._out(y, host)
+
+    def limiting_hessian_apply(self, v):
+        """B^T (c_q B v), no constraint handling (operator.py:514-533)."""
+        self._need_lim()
+        vt, host = self._in(v)
+        y = _torch().empty_like(vt)
+        _lib.check(self.lib.tmop_limiting_apply(self._ctx, _lib.ptr(vt), _lib.ptr(y)), "tmop_limiting_apply")
+        return self._out(y, host)
 
     # ---------------------------------------------------------- raw C-ABI
     @property

@@ -67,6 +67,29 @@ def operator_case(name, dim, counts, order, n_quad, metric, target="unit",
     return p, x
 
 
+def limiting_nodal_case(name, dim, counts, order, n_quad, metric, weight):
+    """Limiting with a NODAL delta and a perturbed reference (operator.py:463-533):
+    the full operator plus limiting_value / limiting_gradient /
+    limiting_hessian_apply on their own."""
+    mesh = tb.build_box(dim, counts, order)
+    rng = np.random.default_rng(SEED + 7)
+    x0 = perturbed_mesh_vector(mesh, rng, 0.1)
+    delta = 0.3 + 0.2 * rng.random(mesh.n_nodes)
+    x = perturbed_mesh_vector(mesh, rng, 0.2)
+    v = rng.standard_normal(x.shape)
+    lim = tb.LimitingConfig(reference=x0, delta=delta, weight=weight)
+    cfg = tb.ObjectiveConfig(metric=tb.MetricId(metric), target=tb.TargetSpec(tb.TargetKind.IDEAL_UNIT),
+                             limiting=lim)
+    p = tb.TmopProblem(mesh, cfg, n_quad)
+    qd = p.hessian_setup(x)
+    out = dict(dim=dim, counts=np.array(counts), order=order, n_quad=n_quad, metric=metric, x=x, v=v,
+               lim_reference=x0, lim_delta_nodal=delta, lim_weight=weight,
+               apply=p.hessian_apply(qd, v), gradient=p.gradient(x), objective=p.objective(x),
+               diagonal=p.hessian_diagonal(qd), lim_value=p.limiting_value(x), lim_gradient=p.limiting_gradient(x),
+               lim_apply=p.limiting_hessian_apply(v))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+
+
 def newton_case(name, dim, counts, order, n_quad, metric, iters, amplitude=0.2,
                 precond=True):
     mesh = tb.build_box(dim, counts, order)
@@ -156,6 +179,8 @@ def main():
     operator_case("op2d_p2_q3_mu55", 2, (3, 3), 2, 3, 55)
     operator_case("op2d_p2_q3_mu55_lim", 2, (2, 2), 2, 3, 55, limiting=(0.4, 1.0))
     operator_case("op3d_p2_q3_mu55_lim", 3, (2, 2, 2), 2, 3, 55, limiting=(0.4, 1.5))
+    limiting_nodal_case("limnodal3d_p2_q4_mu303", 3, (3, 2, 3), 2, 4, 303, 1.7)
+    limiting_nodal_case("limnodal2d_p3_q5_mu2", 2, (3, 4), 3, 5, 2, 0.8)
     newton_case("newton_c1_2d_q2_16x16_mu2", 2, (16, 16), 2, 4, 2, iters=5)
     newton_case("newton_3d_p2_4c_mu303", 3, (4, 4, 4), 2, 4, 303, iters=3)
     newton_case("newton_3d_p1_4c_mu303_noprec", 3, (4, 4, 4), 1, 3, 303, iters=2,

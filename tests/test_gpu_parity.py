@@ -28,12 +28,16 @@ def make(g):
     import paper_2205_12721_b200 as P
     mesh = P.build_box(int(g["dim"]), tuple(int(c) for c in g["counts"]), int(g["order"]))
     kind = P.TargetKind.IDEAL_UNIT if int(g["target"]) == 0 else P.TargetKind.IDEAL_EQUAL_SIZE
+    lim = None
+    if "lim_delta" in g:   # make_golden.py: reference = the uniform lattice
+        lim = P.LimitingConfig(reference=mesh.dof_vector(), delta=float(g["lim_delta"]),
+                               weight=float(g["lim_weight"]))
     cfg = P.ObjectiveConfig(P.MetricId(int(g["metric"])), P.TargetSpec(kind),
-                            spatial_weight=float(g["spatial_weight"]))
+                            spatial_weight=float(g["spatial_weight"]), limiting=lim)
     return P.TmopProblem(mesh, cfg, int(g["n_quad"]))
 
 
-OPS = [n for n in golden_names("op") if not n.endswith("_lim")]
+OPS = golden_names("op")
 
 
 @pytest.mark.parametrize("name", OPS)
@@ -342,3 +346,48 @@ def test_pipelined_host_apply_is_bitwise_equal(order, nq, counts, slabs, rng, mo
     assert torch.equal(got, ref)
     got2 = p.hessian_apply(qd, vh)
     assert torch.equal(got2, ref)
+
+
+@pytest.mark.parametrize("dim,order,nq,counts", [(3, 2, 4, (3, 2, 3)), (2, 3, 5, (3, 4)), (3, 1, 3, (4, 3, 2))])
+def test_limiting_term_matches_oracle(dim, order, nq, counts, rng):
+    """Displacement limiting (operator.py:463-533) with a NODAL delta: the
+    full operator and the limiting-only entry points against the oracle."""
+    import paper_2205_12721_b200 as P
+    om = O.box_mesh(dim, counts, order)
+    x0 = O.perturb(om, rng, 0.1)
+    delta = 0.3 + 0.2 * rng.random(om.n_nodes)
+    metric = O.MU_303 if dim == 3 else O.MU_2
+    oprob = O.OracleProblem(om, metric, nq, limiting={"reference": x0, "delta": delta, "weight": 1.7})
+    mesh = P.build_box(dim, counts, order)
+    lim = P.LimitingConfig(reference=x0, delta=delta, weight=1.7)
+    prob = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId(metric), P.TargetSpec(P.TargetKind.IDEAL_UNIT),
+                                                 limiting=lim), nq)
+    x = O.perturb(om, rng, 0.2)
+    v = rng.standard_normal(x.shape)
+    qd, oq = prob.hessian_setup(x), oprob.hessian_setup(x)
+    assert rel(prob.hessian_apply(qd, v), oprob.hessian_apply(oq, v)) <= TOL
+    assert rel(prob.gradient(x), oprob.gradient(x)) <= TOL
+    assert rel(prob.hessian_diagonal(qd), oprob.hessian_diagonal(oq)) <= TOL
+    assert prob.objective(x) == pytest.approx(oprob.objective(x), rel=TOL)
+    assert prob.limiting_value(x) == pytest.approx(oprob.limiting_value(x), rel=TOL)
+    assert rel(prob.limiting_gradient(x), oprob._lim_grad2(oprob._x2(x)).ravel()) <= TOL
+    assert rel(prob.limiting_hessian_apply(v), oprob._lim_hess2(oprob._x2(v)).ravel()) <= TOL
+
+
+@pytest.mark.parametrize("name", golden_names("limnodal"))
+def test_limiting_nodal_delta_matches_reference_golden(name):
+    import paper_2205_12721_b200 as P
+    g = load_golden(name)
+    mesh = P.build_box(int(g["dim"]), tuple(int(c) for c in g["counts"]), int(g["order"]))
+    lim = P.LimitingConfig(reference=g["lim_reference"], delta=g["lim_delta_nodal"], weight=float(g["lim_weight"]))
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId(int(g["metric"])), P.TargetSpec(P.TargetKind.IDEAL_UNIT),
+                                              limiting=lim), int(g["n_quad"]))
+    x, v = g["x"], g["v"]
+    qd = p.hessian_setup(x)
+    assert rel(p.hessian_apply(qd, v), g["apply"]) <= TOL
+    assert rel(p.gradient(x), g["gradient"]) <= TOL
+    assert p.objective(x) == pytest.approx(float(g["objective"]), rel=TOL)
+    assert rel(p.hessian_diagonal(qd), g["diagonal"]) <= TOL
+    assert p.limiting_value(x) == pytest.approx(float(g["lim_value"]), rel=TOL)
+    assert rel(p.limiting_gradient(x), g["lim_gradient"]) <= TOL
+    assert rel(p.limiting_hessian_apply(v), g["lim_apply"]) <= TOL

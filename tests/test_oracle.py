@@ -188,3 +188,23 @@ def test_yardstick_matches_survey():
     b, f = O.apply_yardstick(3, 2, 4, 160 ** 3, n_dofs)
     assert b / n_dofs == pytest.approx(485, rel=0.01)
     assert f / n_dofs == pytest.approx(1230, rel=0.01)
+
+
+@pytest.mark.parametrize("name", golden_names("limnodal"))
+def test_limiting_nodal_delta_matches_reference(name):
+    """Nodal delta + perturbed reference: the oracle's limiting term
+    (value, raw gradient, raw action) and the full operator against the
+    reference (operator.py:463-533)."""
+    g = load_golden(name)
+    mesh = O.box_mesh(int(g["dim"]), tuple(g["counts"]), int(g["order"]))
+    lim = dict(reference=g["lim_reference"], delta=g["lim_delta_nodal"], weight=float(g["lim_weight"]))
+    p = O.OracleProblem(mesh, int(g["metric"]), int(g["n_quad"]), limiting=lim)
+    x, v = g["x"], g["v"]
+    qd = p.hessian_setup(x)
+    assert rel(p.hessian_apply(qd, v), g["apply"]) <= 1e-12
+    assert rel(p.gradient(x), g["gradient"]) <= 1e-12
+    assert p.objective(x) == pytest.approx(float(g["objective"]), rel=1e-12)
+    assert rel(p.hessian_diagonal(qd), g["diagonal"]) <= 1e-12
+    assert p.limiting_value(x) == pytest.approx(float(g["lim_value"]), rel=1e-12)
+    assert rel(p._lim_grad2(p._x2(x)).ravel(), g["lim_gradient"]) <= 1e-12
+    assert rel(p._lim_hess2(p._x2(v)).ravel(), g["lim_apply"]) <= 1e-12
