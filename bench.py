@@ -215,6 +215,55 @@ def run_order(order, n, nq, steps, warmup, device, with_e2e=False, with_newton=F
     return res, clocks
 
 
+def small_config_c2(steps=200):
+    """BASELINE configs[1] (C2): 3D Q1 perturbed cube 32^3, mu_302 (non-template
+    Hessian), n_q = 3 -- 107,811 DOFs, launch-latency territory.  Eager
+    applies vs a CUDA graph replaying `steps` applies (element kernel + E->L)."""
+    import torch
+
+    import paper_2205_12721_b200 as P
+    from paper_2205_12721_b200 import _lib
+    mesh = P.build_box(3, (32, 32, 32), 1)
+    prob = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_302, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), 3)
+    x = torch.from_numpy(perturbed_x(mesh)).cuda()
+    v = torch.from_numpy(np.random.default_rng(1).standard_normal(mesh.n_dofs)).cuda()
+    y = torch.empty_like(v)
+    qd = prob.hessian_setup(x)
+    for _ in range(5):
+        prob.hessian_apply(qd, v, out=y)
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(steps):
+        prob.hessian_apply(qd, v, out=y)
+    e1.record(s)
+    torch.cuda.synchronize()
+    t_eager = e0.elapsed_time(e1) / 1e3 / steps
+    side = torch.cuda.Stream()
+    side.wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        prob._sync_stream()
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(steps):
+                _lib.check(prob.lib.tmop_hessian_apply(prob.ctx, _lib.ptr(qd.data), _lib.ptr(v), _lib.ptr(y)),
+                           "tmop_hessian_apply")
+    s.wait_stream(side)
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record(s)
+    g.replay()
+    e1.record(s)
+    torch.cuda.synchronize()
+    t_graph = e0.elapsed_time(e1) / 1e3 / steps
+    prob._sync_stream()
+    return {"workload": "C2: 3D Q1 perturbed cube 32^3 elements, mu_302, n_q=3", "n_dofs": mesh.n_dofs,
+            "us_per_apply_eager": 1e6 * t_eager, "gdofs_eager": mesh.n_dofs / t_eager / 1e9,
+            "us_per_apply_graph": 1e6 * t_graph, "gdofs_graph": mesh.n_dofs / t_graph / 1e9,
+            "graph_applies": steps}
+
+
 def newton_iteration(prob, x):
     """One Newton iteration, paper protocol (MINRES fixed at 20 iterations,
     PAPER.md:1002-1004): setup + diagonal + MINRES + line search."""
@@ -458,6 +507,7 @@ def main():
     }
     if "newton" in head:
         line["newton_iteration"] = head["newton"]
+    line["c2_small"] = small_config_c2()
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(HEADLINE_P, 40)
     print(json.dumps(line))

@@ -133,7 +133,7 @@ int tmop_hessian_apply_gather(tmop_ctx *ctx, const double *v, double *y);
 
 /* Streaming pieces of the same action for host-resident pipelines
  * (H2D of v / element kernel / E->L / D2H of y overlapped slab by slab):
- * the element kernel over elements [e_begin, e_end) (e_begin % 8 == 0;
+ * the element kernel over elements [e_begin, e_end) (e_begin % 16 == 0;
  * reads v at those elements' nodes only), and the E->L sum + constraint
  * fix-up for nodes [n_begin, n_end) (every element holding those nodes must
  * have been processed).  Results are bitwise identical to

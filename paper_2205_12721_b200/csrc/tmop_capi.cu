@@ -222,8 +222,8 @@ int tmop_ctx_create(tmop_ctx **out, int dim, int order, int n_quad, int64_t n_el
   c->inv_s = inv_scale;
   c->stream = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
-  // E-vector: element count padded to whole 8-element groups (interleaved layout)
-  const size_t esz = (size_t)((n_elements + 7) / 8 * 8) * dim * np;
+  // E-vector: element count padded to whole 16-element groups (interleaved layout)
+  const size_t esz = (size_t)((n_elements + 15) / 16 * 16) * dim * np;
   e = cudaMalloc(&c->E, (esz ? esz : 1) * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->part_sum, GRID_CAP * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->part_min, GRID_CAP * sizeof(double));
@@ -423,15 +423,15 @@ int tmop_hessian_apply_elements_range(tmop_ctx *c, const double *qdata, const do
                                       int64_t e_end) {
   if (!c || !qdata || !v) return fail(TMOP_ERR_ARG, "NULL argument");
   if (c->lim_on) return fail(TMOP_ERR_ARG, "range apply does not support the limiting term");
-  if (e_begin < 0 || e_end > c->ne || e_begin > e_end || (e_begin & 7))
-    return fail(TMOP_ERR_ARG, "element range [%lld, %lld) invalid (begin must be a multiple of 8, end <= %lld)",
+  if (e_begin < 0 || e_end > c->ne || e_begin > e_end || (e_begin & 15))
+    return fail(TMOP_ERR_ARG, "element range [%lld, %lld) invalid (begin must be a multiple of 16, end <= %lld)",
                 (long long)e_begin, (long long)e_end, (long long)c->ne);
   if (e_begin == e_end) return TMOP_OK;
   ElemArgs a = base_args(c);
   a.in = v;
   a.qdata = qdata + e_begin * tmop_qdata_stride(c);
   a.restr = c->restr + e_begin * c->NP;
-  a.E = c->E + e_begin * c->dim * c->NP;   // (element groups of 8 stay aligned: e_begin % 8 == 0)
+  a.E = c->E + e_begin * c->dim * c->NP;   // (element groups stay aligned: e_begin % 16 == 0)
   a.ne = e_end - e_begin;
   return run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
 }

@@ -62,17 +62,20 @@ __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * i
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int cclamp(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-// Element-group size of the 3D x-line kernels (tmop_xl.cuh): 8 elements per
-// CTA for p <= 2, 4 for p >= 3 (shared-memory budget).
-__host__ __device__ constexpr int xl_epb(int n1) { return n1 <= 3 ? 8 : 4; }
+// Element-group size of the 3D x-line kernels (tmop_xl.cuh): 16 elements per
+// CTA for p = 1 (9 lines per element: 144 threads), 8 for p = 2, 4 for
+// p >= 3 (shared-memory budget).
+__host__ __device__ constexpr int xl_epb(int n1) { return n1 <= 2 ? 16 : (n1 == 3 ? 8 : 4); }
 
 // Element stride of the lean Q-data record (doubles): the smallest value
-// >= fields * points with stride == 16 / epb (mod 16).  Even, so every
-// element block is 16-byte aligned (TMA bulk copies), and with that residue
-// the epb element-interleaved threads of a half-warp reading the same
-// field / slot of consecutive staged elements hit distinct bank pairs.
+// >= fields * points with stride == 16 / epb (mod 16) (2 for epb = 16).
+// Even, so every element block is 16-byte aligned (TMA bulk copies), and
+// with that residue the epb element-interleaved threads of a half-warp
+// reading the same field / slot of consecutive staged elements hit distinct
+// bank pairs (2-way for epb = 16, where an odd stride would break the TMA
+// alignment).
 __host__ __device__ constexpr int lean_stride(int n, int epb) {
-  return n + ((16 + 16 / epb - n % 16) % 16);
+  return n + ((16 + (epb >= 16 ? 2 : 16 / epb) - n % 16) % 16);
 }
 
 template <int DIM, int N, int Q>

@@ -46,8 +46,8 @@ int launch_xl(ElemArgs &a, const Tab &t, cudaStream_t s) {
   using XC = XlCfg<N, Q>;
   constexpr int smem = XC::template smem<KIND>();
   a.ngroups = (a.ne + XC::EPB - 1) / XC::EPB;
-  static_assert(XC::EPB == 8 || XC::EPB == 4, "e_es assumes 4- or 8-element groups");
-  if constexpr (xl_backward<KIND>()) a.e_es = XC::EPB == 8 ? 3 : 2;
+  static_assert(XC::EPB == 16 || XC::EPB == 8 || XC::EPB == 4, "e_es assumes 4-, 8- or 16-element groups");
+  if constexpr (xl_backward<KIND>()) a.e_es = XC::EPB == 16 ? 4 : XC::EPB == 8 ? 3 : 2;
   auto kfn = xl_kernel<N, Q, KIND>;
   static int per_sm = 0;
   if (per_sm == 0) {

@@ -64,9 +64,12 @@ __host__ __device__ constexpr bool xl_qdata() {
 template <int N, int Q>
 struct XlPad {
   static constexpr int EPB = xl_epb(N);
-  static constexpr int U_QZ = EPB == 8 ? (N * N) | (Q & 1) : (N == 4 ? (Q % 4 == 0 ? 16 : 17) : 25);
-  static constexpr int W_QY = EPB == 8 ? (N | 1) : ((N == 5 && (Q == 3 || Q == 7)) ? 7 : 5);
-  static constexpr int W_QZ = EPB == 8 ? Q * W_QY + ((N & 1) && !(Q & 1) ? 1 : 0)
+  // EPB = 16: a half-warp is one item x 16 elements -- conflict-free unpadded
+  static constexpr int U_QZ = EPB == 16 ? N * N
+                            : EPB == 8 ? (N * N) | (Q & 1) : (N == 4 ? (Q % 4 == 0 ? 16 : 17) : 25);
+  static constexpr int W_QY = EPB == 16 ? N : EPB == 8 ? (N | 1) : ((N == 5 && (Q == 3 || Q == 7)) ? 7 : 5);
+  static constexpr int W_QZ = EPB == 16 ? Q * N
+                            : EPB == 8 ? Q * W_QY + ((N & 1) && !(Q & 1) ? 1 : 0)
                                        : (N == 4 ? Q * 5 : (Q == 3 ? 21 : Q == 4 ? 21 : Q == 6 ? 33 : Q * W_QY));
 };
 

@@ -467,7 +467,7 @@ class TmopProblem:
             return (ex * p + p) + NX * ((ey * p + p) + NY * (ez * p + p)) + 1
 
         ns = min(self.pipeline_slabs, nz)
-        bounds = [((k * nz) // ns) * layer // 8 * 8 for k in range(ns)] + [ne]
+        bounds = [((k * nz) // ns) * layer // 16 * 16 for k in range(ns)] + [ne]
         copied, done = 0, 0
         for k in range(ns):
             e0, e1 = bounds[k], bounds[k + 1]
