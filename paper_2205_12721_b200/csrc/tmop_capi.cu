@@ -211,8 +211,12 @@ int tmop_ctx_create(tmop_ctx **out, int dim, int order, int n_quad, int64_t n_el
   c->l2e_idx = l2e_index;
   for (int q = 0; q < n_quad; ++q) {
     for (int i = 0; i < c->n1; ++i) {
-      c->tab.B[q * c->n1 + i] = B[q * c->n1 + i];
-      c->tab.G[q * c->n1 + i] = G[q * c->n1 + i];
+      const double b = B[q * c->n1 + i], g = G[q * c->n1 + i];
+      c->tab.B[q * c->n1 + i] = b;
+      c->tab.G[q * c->n1 + i] = g;
+      c->tab.P[0][q * c->n1 + i] = b * b;
+      c->tab.P[1][q * c->n1 + i] = b * g;
+      c->tab.P[2][q * c->n1 + i] = g * g;
     }
     c->tab.w1[q] = w1[q];
   }

@@ -24,6 +24,9 @@ struct Tab {
   double B[MAXQ * MAXN];
   double G[MAXQ * MAXN];
   double w1[MAXQ];
+  // elementwise products B.B, B.G, G.G (the diagonal's per-axis tables,
+  // operator.py:443-448), indexed like B
+  double P[3][MAXQ * MAXN];
 };
 
 template <int Q, int N>
