@@ -264,6 +264,24 @@ def small_config_c2(steps=200):
             "graph_applies": steps}
 
 
+# Kershaw eps=0.3, 24^3, n_q=9, mu_303, Jacobi-MINRES,
+# GPU-PA* time to solution on 4x V100 and its Newton / MINRES iteration counts.
+PAPER_KERSHAW = {1: (0.4, 11, 203), 2: (0.9, 18, 507), 3: (3.9, 41, 1536), 4: (8.5, 70, 3110)}
+
+
+def kershaw_paper_table(orders=(1, 2, 3, 4)):
+    """The paper's time-to-solution table on ONE B200 (tools/kershaw_solve.py)."""
+    from tools.kershaw_solve import solve
+    out = []
+    for p in orders:
+        r = solve(p, 24, 9)
+        t, nn, nm = PAPER_KERSHAW[p]
+        r.update(paper_gpu_pa_star_s_4xV100=t, paper_newton_iterations=nn, paper_minres_iterations=nm,
+                 speedup_vs_paper=t / r["solve_s"])
+        out.append(r)
+    return out
+
+
 def newton_iteration(prob, x):
     """One Newton iteration, paper protocol (MINRES fixed at 20 iterations,
     PAPER.md:1002-1004): setup + diagonal + MINRES + line search."""
@@ -508,6 +526,8 @@ def main():
     if "newton" in head:
         line["newton_iteration"] = head["newton"]
     line["c2_small"] = small_config_c2()
+    if not args.no_newton:
+        line["kershaw_paper_table"] = kershaw_paper_table()
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(HEADLINE_P, 40)
     print(json.dumps(line))
