@@ -115,9 +115,11 @@ struct Cfg {
   // Launch shape, from the A/B sweep of round 1 (profiles/round1_apply_ab.md):
   // 128-thread CTAs with ~56 KB (4 CTAs / SM) for p = 1, 2, 4; 256-thread
   // CTAs with ~72 KB (3 CTAs / SM) for p = 3.
-  static constexpr bool WIDE = false;   // 256-thread variant (was best for p=3 before the gather prefetch)
+  // 256-thread CTAs for n_q >= 7 (one element's Q-data + work arrays fill the
+  // CTA's shared memory; measured 1.4-1.8x faster at n_q = 9, round 1)
+  static constexpr bool WIDE = Q >= 7;
   static constexpr int NT = TMOP_ELEM_NT ? TMOP_ELEM_NT : (WIDE ? 256 : 128);
-  static constexpr int MINB = TMOP_MIN_BLOCKS ? TMOP_MIN_BLOCKS : (WIDE ? 3 : 4);
+  static constexpr int MINB = TMOP_MIN_BLOCKS ? TMOP_MIN_BLOCKS : (WIDE ? 1 : 4);
   static constexpr int BUDGET = TMOP_SMEM_BUDGET ? TMOP_SMEM_BUDGET : (WIDE ? 9216 : 7168);
   // elements per CTA: work arrays + staged Q-data within BUDGET doubles
   static constexpr int EPB = cclamp(BUDGET / (PER + QS), 1, 32);
