@@ -38,7 +38,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(out.splitlines()))
 hdr = rows[1]
 ix = {h: i for i, h in enumerate(hdr)}
-st, ins = collections.Counter(), collections.Counter()
+st, ins, exc = collections.Counter(), collections.Counter(), collections.Counter()
 base = None
 for r in rows[2:]:
     if len(r) < len(hdr):
@@ -52,7 +52,11 @@ for r in rows[2:]:
         line = line.split(" < ")[0]
     st[line] += float(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
     ins[line] += float(r[ix["Instructions Executed"]] or 0)
-ts, ti = sum(st.values()), sum(ins.values())
-print(f"{'line':40s} {'stall%':>7s} {'inst%':>7s}")
+    try:
+        exc[line] += float(r[ix["L1 Wavefronts Shared Excessive"]] or 0)
+    except (KeyError, ValueError):
+        pass
+ts, ti, te = sum(st.values()), sum(ins.values()), max(sum(exc.values()), 1)
+print(f"{'line':40s} {'stall%':>7s} {'inst%':>7s} {'smem-excess%':>12s}")
 for line, s in st.most_common(top):
-    print(f"{line:40s} {s / ts * 100:7.2f} {ins[line] / ti * 100:7.2f}")
+    print(f"{line:40s} {s / ts * 100:7.2f} {ins[line] / ti * 100:7.2f} {exc[line] / te * 100:12.2f}")
