@@ -110,6 +110,22 @@ def newton_case(name, dim, counts, order, n_quad, metric, iters, amplitude=0.2,
                         initial_grad_norm=res.initial_grad_norm)
 
 
+def kershaw_newton_case(name, counts, order, n_quad, iters):
+    """The paper benchmark's flow at a small size (bench.py:170-245): Kershaw
+    eps 0.3 mesh, mu_303 ideal shape, Jacobi-MINRES Newton, fixed iterations."""
+    spec = tb.MeshSpec(dim=3, nx=counts[0], ny=counts[1], nz=counts[2], order=order)
+    mesh = tb.apply_kershaw(tb.build_cartesian(spec), 0.3, 0.3)
+    x0 = mesh.dof_vector()
+    p = tb.TmopProblem(mesh, tb.ObjectiveConfig(tb.MetricId.MU_303, tb.TargetSpec(tb.TargetKind.IDEAL_UNIT)),
+                       n_quad)
+    res = tb.newton_solve(x0, p, tb.NewtonConfig(max_iterations=iters), tb.MinresConfig(preconditioned=True))
+    recs = np.array([[r.alpha, r.objective, r.grad_norm, r.minres_iterations,
+                      r.minres_rel_residual, r.min_det] for r in res.trace.records])
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), counts=np.array(counts), order=order, n_quad=n_quad,
+                        iters=iters, x0=x0, x=res.x, records=recs, f0=p.objective(x0),
+                        f_final=p.objective(res.x), success=res.success)
+
+
 def minres_case(name, n=40, seed=7):
     """Small dense symmetric indefinite system with Jacobi (sol:93-180)."""
     rng = np.random.default_rng(seed)
@@ -185,6 +201,7 @@ def main():
     newton_case("newton_3d_p2_4c_mu303", 3, (4, 4, 4), 2, 4, 303, iters=3)
     newton_case("newton_3d_p1_4c_mu303_noprec", 3, (4, 4, 4), 1, 3, 303, iters=2,
                 precond=False)
+    kershaw_newton_case("kershawnewton_6x4x4_p2_q4", (6, 4, 4), 2, 4, 100)
     minres_case("minres_dense")
     minres_conditioned_case("minres_wellcond")
     metric_points("metric_points")
