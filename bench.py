@@ -428,6 +428,12 @@ def run_distributed(args, rank, world, local, device, metric, config):
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (perturbed slabs, seeded)",
                 "config": cfg, "halo_ms_per_step": 1e3 * halo,
                 "halo_bytes_per_neighbor": dp.halo.bytes_per_exchange,
+                "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peaks()[0],
+                             "achieved": apply_bytes(3, HEADLINE_P, nq, mesh.n_elements, mesh.n_dofs)
+                             / (total / args.steps - halo) / 1e9,
+                             "frac": apply_bytes(3, HEADLINE_P, nq, mesh.n_elements, mesh.n_dofs)
+                             / (total / args.steps - halo) / 1e9 / peaks()[0],
+                             "traffic": None, "kernel": "local Hessian action (element kernel + E->L), per GPU"},
                 "e2e": {"value": global_dofs / te / 1e9, "unit": "GDOF/s",
                         "h2d_bytes_per_step": 8 * mesh.n_dofs * world, "d2h_bytes_per_step": 8 * mesh.n_dofs * world},
                 "gpu_launches": 2 * args.steps, "clocks": cs.summary()}
@@ -443,6 +449,7 @@ def main():
     ap.add_argument("--orders", default="1,2,3,4", help="orders reported under per_order")
     ap.add_argument("--no-newton", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-dist", action="store_true", help="run the z-slab (NCCL) path even with one rank")
     args = ap.parse_args()
     rank, world, local = dist_env()
     n_h, nq_h = ORDERS[HEADLINE_P]
@@ -465,13 +472,14 @@ def main():
         return
 
     import torch
-    if world > 1:
+    dist_path = world > 1 or args.force_dist
+    if dist_path:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
-    device = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
+    device = torch.device("cuda", local if dist_path else torch.cuda.current_device())
     torch.cuda.set_device(device)
-    if world > 1:
+    if dist_path:
         torch.distributed.barrier()
         run_distributed(args, rank, world, local, device, metric, config)
         torch.distributed.destroy_process_group()
