@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -60,6 +61,11 @@ struct tmop_ctx {
   const double *lim_x0, *lim_dn;
   double lim_delta, lim_weight;
   double *E2, *lim_y, *lim_val;
+  // overlapped apply (tmop_hessian_apply on lattices): E->L of finished slabs
+  // runs on a second stream while the element kernel works on the next slab
+  cudaStream_t s2;
+  cudaEvent_t ev[33];
+  int ov_slabs;
   double *hist;      // MINRES residual history (device, optional)
   int hist_cap;
 };
@@ -225,6 +231,11 @@ int tmop_ctx_create(tmop_ctx **out, int dim, int order, int n_quad, int64_t n_el
   c->det_w = det_w;
   c->inv_s = inv_scale;
   c->stream = (cudaStream_t)stream;
+  {
+    const char *ev = getenv("TMOP_APPLY_SLABS");
+    c->ov_slabs = ev ? atoi(ev) : 8;
+    if (c->ov_slabs > 30) c->ov_slabs = 30;
+  }
   cudaError_t e = cudaSuccess;
   // E-vector: element count padded to whole 16-element groups (interleaved layout)
   const size_t esz = (size_t)((n_elements + 15) / 16 * 16) * dim * np;
@@ -252,6 +263,10 @@ int tmop_ctx_destroy(tmop_ctx *c) {
   cudaFree(c->vpart1);
   cudaFree(c->vpart2);
   cudaFree(c->flag);
+  if (c->s2) {
+    for (int i = 0; i < 33; ++i) cudaEventDestroy(c->ev[i]);
+    cudaStreamDestroy(c->s2);
+  }
   cudaFree(c->E2);
   cudaFree(c->lim_y);
   cudaFree(c->lim_val);
@@ -405,8 +420,60 @@ int tmop_hessian_setup(tmop_ctx *c, const double *x, double *qdata, tmop_det_sta
   return TMOP_OK;
 }
 
+// Overlapped action on a verified lattice: z-slab element launches on the
+// context stream; after each, the E->L sum of the node planes that slab
+// completes (ascending element order per node, as the one-shot gather) runs
+// on a second stream in small CTAs that fit beside the persistent element
+// kernel (register headroom), so the memory-bound gather hides under the
+// FP64-bound element work.  Results are bitwise identical to the one-shot path.
+static int apply_overlapped(tmop_ctx *c, const double *qdata, const double *v, double *y) {
+  if (!c->s2) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
+    for (int i = 0; i < 33; ++i) CUDA_TRY(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
+  }
+  const int64_t layer = (int64_t)c->lat_n[0] * c->lat_n[1];
+  const int64_t plane = ((int64_t)c->lat_n[0] * c->lat_p + 1) * ((int64_t)c->lat_n[1] * c->lat_p + 1);
+  const int nz = c->lat_n[2];
+  const int ns = c->ov_slabs < nz ? c->ov_slabs : nz;
+  const E2LMap m0 = e2l_map(c);
+  CUDA_TRY(cudaEventRecord(c->ev[31], c->stream));        // fork: s2 follows everything before this call
+  CUDA_TRY(cudaStreamWaitEvent(c->s2, c->ev[31], 0));
+  int64_t done = 0;
+  for (int k = 0; k < ns; ++k) {
+    const int64_t e0 = ((int64_t)k * nz / ns) * layer / 16 * 16;
+    const int64_t e1 = k + 1 == ns ? c->ne : ((int64_t)(k + 1) * nz / ns) * layer / 16 * 16;
+    if (e1 > e0) {
+      ElemArgs a = base_args(c);
+      a.in = v;
+      a.qdata = qdata + e0 * tmop_qdata_stride(c);
+      a.restr = c->restr + e0 * c->NP;
+      a.E = c->E + e0 * c->dim * c->NP;
+      a.ne = e1 - e0;
+      int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
+      if (rc) return rc;
+    }
+    const int64_t fin = e1 == c->ne ? c->nn : (e1 / layer) * c->lat_p * plane;
+    if (fin > done) {
+      CUDA_TRY(cudaEventRecord(c->ev[k], c->stream));
+      CUDA_TRY(cudaStreamWaitEvent(c->s2, c->ev[k], 0));
+      E2LMap m = m0;
+      m.es = c->e_es;
+      launch_e2l(c->dim, c->nn, m, c->E, c->fixed, 0, v, nullptr, y, c->s2, done, fin, 128);
+      CUDA_TRY(cudaGetLastError());
+      done = fin;
+    }
+  }
+  CUDA_TRY(cudaEventRecord(c->ev[32], c->s2));            // join
+  CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev[32], 0));
+  return TMOP_OK;
+}
+
 int tmop_hessian_apply(tmop_ctx *c, const double *qdata, const double *v, double *y) {
   if (!c || !qdata || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
+  // (p <= 3: the x-line element kernel leaves register room for the gather's
+  // CTAs; measured 4-5 % faster there, slower at p = 4)
+  if (c->lat_p > 0 && c->n1 <= 4 && !c->lim_on && c->ov_slabs > 1 && c->ne >= (int64_t)c->ov_slabs * 4096)
+    return apply_overlapped(c, qdata, v, y);
   int rc = tmop_hessian_apply_elements(c, qdata, v);
   if (rc) return rc;
   return tmop_hessian_apply_gather(c, v, y);

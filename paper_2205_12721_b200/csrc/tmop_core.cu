@@ -128,9 +128,8 @@ __global__ void e2l_kernel(int64_t nn, int64_t n0, int64_t n1, const E2LMap m, c
 }
 
 int launch_e2l(int dim, int64_t nn, const E2LMap &m, const double *E, const uint8_t *fixed, int mode, const double *v,
-               const double *add, double *y, cudaStream_t s, int64_t n0, int64_t n1) {
+               const double *add, double *y, cudaStream_t s, int64_t n0, int64_t n1, int nt) {
   if (n1 < 0) n1 = nn;
-  const int nt = 256;
   const int64_t grid = (n1 - n0 + nt - 1) / nt;
   if (grid <= 0) return 0;
   if (dim == 2)

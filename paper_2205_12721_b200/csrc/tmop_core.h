@@ -30,7 +30,7 @@ struct E2LMap {
 };
 // Node range [n0, n1) (n1 < 0: all nodes).
 int launch_e2l(int dim, int64_t nn, const E2LMap &m, const double *E, const uint8_t *fixed, int mode, const double *v, const double *add, double *y, cudaStream_t s,
-               int64_t n0 = 0, int64_t n1 = -1);
+               int64_t n0 = 0, int64_t n1 = -1, int nt = 256);
 void launch_fin(int nparts, const double *psum, const double *pmin, const int64_t *parg, double sum_scale,
                 double *sum_out, double add_scale, const double *add, tmop_det_status *det_out, cudaStream_t s);
 int launch_metric_eval(int metric, int dim, int64_t n, const double *T, double *mu, double *P, double *H);
