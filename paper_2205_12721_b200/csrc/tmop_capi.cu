@@ -243,8 +243,8 @@ int tmop_ctx_create(tmop_ctx **out, int dim, int order, int n_quad, int64_t n_el
   if (e == cudaSuccess) e = cudaMalloc(&c->part_sum, GRID_CAP * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->part_min, GRID_CAP * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->part_arg, GRID_CAP * sizeof(int64_t));
-  if (e == cudaSuccess) e = cudaMalloc(&c->vpart1, VEC_GRID_CAP * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&c->vpart2, VEC_GRID_CAP * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c->vpart1, VPART_CAP * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c->vpart2, VPART_CAP * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->flag, sizeof(int));
   if (e != cudaSuccess) {
     tmop_ctx_destroy(c);
@@ -426,11 +426,17 @@ int tmop_hessian_setup(tmop_ctx *c, const double *x, double *qdata, tmop_det_sta
 // on a second stream in small CTAs that fit beside the persistent element
 // kernel (register headroom), so the memory-bound gather hides under the
 // FP64-bound element work.  Results are bitwise identical to the one-shot path.
-static int apply_overlapped(tmop_ctx *c, const double *qdata, const double *v, double *y) {
+static int ensure_s2(tmop_ctx *c) {
   if (!c->s2) {
     CUDA_TRY(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
     for (int i = 0; i < 33; ++i) CUDA_TRY(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
   }
+  return TMOP_OK;
+}
+
+static int apply_overlapped(tmop_ctx *c, const double *qdata, const double *v, double *y) {
+  int rc0 = ensure_s2(c);
+  if (rc0) return rc0;
   const int64_t layer = (int64_t)c->lat_n[0] * c->lat_n[1];
   const int64_t plane = ((int64_t)c->lat_n[0] * c->lat_p + 1) * ((int64_t)c->lat_n[1] * c->lat_p + 1);
   const int nz = c->lat_n[2];
@@ -672,6 +678,55 @@ int tmop_minres_step_op(tmop_ctx *c, const double *qdata, int64_t n, double *Av,
                         double *x, double rtol, tmop_minres_state *st2, int k) {
   if (!c || !qdata || !st2) return fail(TMOP_ERR_ARG, "NULL argument");
   if (n != c->nn * c->dim) return fail(TMOP_ERR_ARG, "vector length %lld != dim * n_nodes", (long long)n);
+  tmop_minres_state *cur = st2 + (k & 1), *nxt = st2 + ((k + 1) & 1);
+  if (c->lat_p > 0 && c->n1 <= 4 && !c->lim_on && c->ov_slabs > 1 && c->ne >= (int64_t)c->ov_slabs * 4096) {
+    // overlapped: element kernel by z-slab on the context stream, the fused
+    // E->L + K1 of each finished node range on the second stream (its K1
+    // partials in a per-slab block of vpart1), then K2 / K3 reduce them all
+    int rc = ensure_s2(c);
+    if (rc) return rc;
+    const int64_t layer = (int64_t)c->lat_n[0] * c->lat_n[1];
+    const int64_t plane = ((int64_t)c->lat_n[0] * c->lat_p + 1) * ((int64_t)c->lat_n[1] * c->lat_p + 1);
+    const int nz = c->lat_n[2];
+    const int ns = c->ov_slabs < nz ? c->ov_slabs : nz;
+    const int gs = VPART_CAP / ns;
+    CUDA_TRY(cudaEventRecord(c->ev[31], c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->s2, c->ev[31], 0));
+    int64_t done = 0;
+    int np1 = 0;
+    for (int s_ = 0; s_ < ns; ++s_) {
+      const int64_t e0 = ((int64_t)s_ * nz / ns) * layer / 16 * 16;
+      const int64_t e1 = s_ + 1 == ns ? c->ne : ((int64_t)(s_ + 1) * nz / ns) * layer / 16 * 16;
+      if (e1 > e0) {
+        ElemArgs a = base_args(c);
+        a.in = v;
+        a.qdata = qdata + e0 * tmop_qdata_stride(c);
+        a.restr = c->restr + e0 * c->NP;
+        a.E = c->E + e0 * c->dim * c->NP;
+        a.ne = e1 - e0;
+        rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
+        if (rc) return rc;
+      }
+      const int64_t fin = e1 == c->ne ? c->nn : (e1 / layer) * c->lat_p * plane;
+      if (fin > done) {
+        CUDA_TRY(cudaEventRecord(c->ev[s_], c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->s2, c->ev[s_], 0));
+        int64_t want = (fin - done + 4 * 128 - 1) / (4 * 128);
+        const int grid = (int)(want < 1 ? 1 : (want > gs ? gs : want));
+        launch_e2l_k1_range(c->nn, done, fin, e2l_map(c), c->E, nullptr, c->fixed, v, r1, Av, cur,
+                            c->vpart1 + np1, grid, c->s2);
+        CUDA_TRY(cudaGetLastError());
+        np1 += grid;
+        done = fin;
+      }
+    }
+    CUDA_TRY(cudaEventRecord(c->ev[32], c->s2));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev[32], 0));
+    launch_minres_k23(n, Av, r2, inv, z, v, w, w1buf, w2, x, rtol, cur, nxt, c->vpart1, np1, c->vpart2, c->hist,
+                      c->hist_cap, c->stream);
+    CUDA_TRY(cudaGetLastError());
+    return TMOP_OK;
+  }
   ElemArgs a = base_args(c);
   a.in = v;
   a.qdata = qdata;
@@ -682,9 +737,8 @@ int tmop_minres_step_op(tmop_ctx *c, const double *qdata, int64_t n, double *Av,
     if (rc) return rc;
   }
   launch_minres_step_op(c->dim, c->nn, e2l_map(c), c->E, c->lim_on ? c->lim_y : nullptr, c->fixed, n, Av, r1, r2,
-                        inv, z, v, w,
-                        w1buf, w2, x, rtol, st2 + (k & 1), st2 + ((k + 1) & 1), c->vpart1, c->vpart2, c->hist,
-                        c->hist_cap, c->stream);
+                        inv, z, v, w, w1buf, w2, x, rtol, cur, nxt, c->vpart1, c->vpart2, c->hist, c->hist_cap,
+                        c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }

@@ -417,10 +417,10 @@ template <bool V2>
 __global__ void __launch_bounds__(VEC_NT) minres_k2(int64_t n, double *__restrict__ Av, const double *__restrict__ r2,
                                                     const double *__restrict__ inv, double *__restrict__ z,
                                                     const tmop_minres_state *cur, const double *__restrict__ part1,
-                                                    double *__restrict__ part2, int np) {
+                                                    int np1, double *__restrict__ part2) {
   if (cur->done) return;
   __shared__ double sv[VEC_NT / 32];
-  const double alfa = reduce_partials(part1, np, sv);
+  const double alfa = reduce_partials(part1, np1, sv);
   const double f = alfa / cur->beta;
   double s = 0.0;
   auto one = [&](int64_t i) {
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(VEC_NT) minres_k3(int64_t n, const double *__r
                                                     const double *__restrict__ w, double *__restrict__ w1buf,
                                                     const double *__restrict__ w2, double *__restrict__ x,
                                                     const tmop_minres_state *cur, tmop_minres_state *nxt,
-                                                    const double *__restrict__ part1,
+                                                    const double *__restrict__ part1, int np1,
                                                     const double *__restrict__ part2, int np, double rtol,
                                                     double *__restrict__ hist, int hist_cap) {
   const tmop_minres_state c = *cur;
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(VEC_NT) minres_k3(int64_t n, const double *__r
     return;
   }
   __shared__ double sv[VEC_NT / 32];
-  const double alfa = reduce_partials(part1, np, sv);
+  const double alfa = reduce_partials(part1, np1, sv);
   const double beta2 = reduce_partials(part2, np, sv);
   tmop_minres_state s = c;
   s.itn = c.itn + 1;
@@ -551,16 +551,17 @@ static bool al16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
 static void launch_k23(int64_t n, double *Av, const double *r2, const double *inv, double *z, double *v,
                        const double *w, double *w1buf, const double *w2, double *x, double rtol,
-                       tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, double *part2, double *hist,
-                       int hist_cap, int g, cudaStream_t s) {
+                       tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, int np1, double *part2,
+                       double *hist, int hist_cap, int g, cudaStream_t s) {
   const bool v2 = al16(Av) && al16(r2) && (!inv || al16(inv)) && al16(z) && al16(v) && al16(w) && al16(w1buf) &&
                   al16(w2) && al16(x);
   if (v2) {
-    minres_k2<true><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, part2, g);
-    minres_k3<true><<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol, hist, hist_cap);
+    minres_k2<true><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, np1, part2);
+    minres_k3<true><<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, np1, part2, g, rtol, hist,
+                                         hist_cap);
   } else {
-    minres_k2<false><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, part2, g);
-    minres_k3<false><<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, part2, g, rtol, hist,
+    minres_k2<false><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, np1, part2);
+    minres_k3<false><<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, np1, part2, g, rtol, hist,
                                           hist_cap);
   }
 }
@@ -570,18 +571,19 @@ static void launch_k23(int64_t n, double *Av, const double *r2, const double *in
 //   Av[i] = (fixed ? v : sum_E) ; Av -= (beta/oldb) r1 (itn >= 2) ; alfa partial v.Av
 // Grid = vec_grid(n), grid-stride over nodes, so the partial array has the
 // same length the following K2 / K3 expect.
-template <int D, bool LAT>
-__global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, const E2LMap m, const double *__restrict__ E,
+template <int D, bool LAT, int NT = VEC_NT>
+__global__ void __launch_bounds__(NT) e2l_minres_k1(int64_t nn, int64_t n0, int64_t n1, const E2LMap m,
+                                                    const double *__restrict__ E,
                                                         const double *__restrict__ add,
                                                         const uint8_t *__restrict__ fixed, const double *__restrict__ v,
                                                         const double *__restrict__ r1, double *__restrict__ Av,
                                                         const tmop_minres_state *cur, double *__restrict__ part) {
   if (cur->done) return;
-  __shared__ double sv[VEC_NT / 32];
+  __shared__ double sv[NT / 32];
   const bool sub = cur->itn >= 1;
   const double f = sub ? cur->beta / cur->oldb : 0.0;
   double s = 0.0;
-  for (int64_t node = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; node < nn; node += (int64_t)gridDim.x * VEC_NT) {
+  for (int64_t node = n0 + (int64_t)blockIdx.x * NT + threadIdx.x; node < n1; node += (int64_t)gridDim.x * NT) {
     double acc[D];
     e2l_node<D, LAT>(node, m, E, acc);
     const uint8_t fl = __ldg(fixed + node);
@@ -595,7 +597,7 @@ __global__ void __launch_bounds__(VEC_NT) e2l_minres_k1(int64_t nn, const E2LMap
       s += vi * y;
     }
   }
-  s = block_sum<VEC_NT>(s, sv);
+  s = block_sum<NT>(s, sv);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
@@ -606,12 +608,29 @@ void launch_minres_step_op(int dim, int64_t nn, const E2LMap &m, const double *E
                            double *part2, double *hist, int hist_cap, cudaStream_t s) {
   const int g = vec_grid(n);
   if (dim == 2)
-    e2l_minres_k1<2, false><<<g, VEC_NT, 0, s>>>(nn, m, E, add, fixed, v, r1, Av, cur, part1);
+    e2l_minres_k1<2, false><<<g, VEC_NT, 0, s>>>(nn, 0, nn, m, E, add, fixed, v, r1, Av, cur, part1);
   else if (m.lat_p > 0)
-    e2l_minres_k1<3, true><<<g, VEC_NT, 0, s>>>(nn, m, E, add, fixed, v, r1, Av, cur, part1);
+    e2l_minres_k1<3, true><<<g, VEC_NT, 0, s>>>(nn, 0, nn, m, E, add, fixed, v, r1, Av, cur, part1);
   else
-    e2l_minres_k1<3, false><<<g, VEC_NT, 0, s>>>(nn, m, E, add, fixed, v, r1, Av, cur, part1);
-  launch_k23(n, Av, r2, inv, z, v, w, w1buf, w2, x, rtol, cur, nxt, part1, part2, hist, hist_cap, g, s);
+    e2l_minres_k1<3, false><<<g, VEC_NT, 0, s>>>(nn, 0, nn, m, E, add, fixed, v, r1, Av, cur, part1);
+  launch_k23(n, Av, r2, inv, z, v, w, w1buf, w2, x, rtol, cur, nxt, part1, g, part2, hist, hist_cap, g, s);
+}
+
+// Overlapped pieces: the fused E->L + K1 over nodes [n0, n1) of a 3D lattice
+// in 128-thread CTAs (partials into part[0 .. grid)), and K2/K3 reducing np1
+// K1 partials.
+void launch_e2l_k1_range(int64_t nn, int64_t n0, int64_t n1, const E2LMap &m, const double *E, const double *add,
+                         const uint8_t *fixed, const double *v, const double *r1, double *Av,
+                         const tmop_minres_state *cur, double *part, int grid, cudaStream_t s) {
+  e2l_minres_k1<3, true, 128><<<grid, 128, 0, s>>>(nn, n0, n1, m, E, add, fixed, v, r1, Av, cur, part);
+}
+
+void launch_minres_k23(int64_t n, double *Av, const double *r2, const double *inv, double *z, double *v,
+                       const double *w, double *w1buf, const double *w2, double *x, double rtol,
+                       tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, int np1, double *part2,
+                       double *hist, int hist_cap, cudaStream_t s) {
+  const int g = vec_grid(n);
+  launch_k23(n, Av, r2, inv, z, v, w, w1buf, w2, x, rtol, cur, nxt, part1, np1, part2, hist, hist_cap, g, s);
 }
 
 void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r2, const double *inv, double *z,
@@ -620,7 +639,7 @@ void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r
                         double *hist, int hist_cap, cudaStream_t s) {
   const int g = vec_grid(n);
   minres_k1<<<g, VEC_NT, 0, s>>>(n, Av, r1, v, cur, part1);
-  launch_k23(n, Av, r2, inv, z, v, w, w1buf, w2, x, rtol, cur, nxt, part1, part2, hist, hist_cap, g, s);
+  launch_k23(n, Av, r2, inv, z, v, w, w1buf, w2, x, rtol, cur, nxt, part1, g, part2, hist, hist_cap, g, s);
 }
 
 }  // namespace tmop

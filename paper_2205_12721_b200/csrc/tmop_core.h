@@ -11,6 +11,7 @@ namespace tmop {
 
 constexpr int VEC_NT = 256;
 constexpr int VEC_GRID_CAP = 148 * 4;
+constexpr int VPART_CAP = 4096;   // vector partials capacity (overlapped K1 slabs need more than one grid)
 
 int vec_grid(int64_t n);
 
@@ -51,6 +52,13 @@ void launch_minres_step_op(int dim, int64_t nn, const E2LMap &m, const double *E
                            double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt, double *part1,
                            double *part2, double *hist, int hist_cap, cudaStream_t s);
 
+void launch_e2l_k1_range(int64_t nn, int64_t n0, int64_t n1, const E2LMap &m, const double *E, const double *add,
+                         const uint8_t *fixed, const double *v, const double *r1, double *Av,
+                         const tmop_minres_state *cur, double *part, int grid, cudaStream_t s);
+void launch_minres_k23(int64_t n, double *Av, const double *r2, const double *inv, double *z, double *v,
+                       const double *w, double *w1buf, const double *w2, double *x, double rtol,
+                       tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, int np1, double *part2,
+                       double *hist, int hist_cap, cudaStream_t s);
 int launch_lattice_check(int64_t ne, int np, const int32_t *restr, int nx, int ny, int nz, int p, int *flag,
                          cudaStream_t s);
 

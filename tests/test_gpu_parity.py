@@ -422,3 +422,31 @@ def test_kershaw_newton_solve_matches_reference(name):
     assert np.abs(np.asarray(res.x) - g["x"]).max() <= 1e-9
     assert np.abs(np.asarray(res.x) - mesh0.dof_vector()).max() <= 1e-9
     assert p.objective(res.x) == pytest.approx(float(g["f_final"]), rel=1e-10)
+
+
+def test_overlapped_apply_and_minres_match_one_shot(rng, monkeypatch):
+    """Lattice meshes with >= 8 x 4096 elements run the Hessian action and the
+    fused MINRES step slab by slab with the E->L on a second stream
+    (TMOP_APPLY_SLABS): the action is bitwise equal to the one-shot path; the
+    MINRES iterate differs only by the K1 partial-sum grouping (1e-12)."""
+    import torch
+
+    import paper_2205_12721_b200 as P
+    counts = (34, 32, 32)
+    om = O.box_mesh(3, counts, 1)
+    x = O.perturb(om, rng, 0.2)
+    v = torch.from_numpy(rng.standard_normal(x.shape)).cuda()
+    out = {}
+    for slabs in ("1", "8"):
+        monkeypatch.setenv("TMOP_APPLY_SLABS", slabs)
+        mesh = P.build_box(3, counts, 1)
+        p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), 3)
+        qd = p.hessian_setup(x)
+        y = p.hessian_apply(qd, v).clone()
+        pre = P.jacobi_preconditioner(p.hessian_diagonal(qd), p.ctx)
+        mr = P.minres(lambda vv: p.hessian_apply(qd, vv), v, P.MinresConfig(max_iterations=20, rel_tolerance=1e-300),
+                      pre, p.ctx, operator=(p, qd))
+        out[slabs] = (y, mr.x.clone(), mr.iterations)
+    assert torch.equal(out["1"][0], out["8"][0])
+    assert out["1"][2] == out["8"][2] == 20
+    assert rel(out["8"][1], out["1"][1].cpu().numpy()) <= 1e-12
