@@ -95,6 +95,11 @@ def test_torch_path_matches_numpy_path_and_is_deterministic():
     (3, 2, 6, O.MU_303, (3, 3, 2)), (3, 3, 9, O.MU_55, (2, 2, 2)),
     (3, 1, 3, O.MU_302, (4, 3, 3)), (3, 2, 4, O.MU_321, (3, 3, 3)), (3, 3, 5, O.MU_302, (2, 2, 3)),
     (2, 2, 4, O.MU_7, (5, 4)), (2, 4, 6, O.MU_2, (3, 3)), (2, 1, 2, O.MU_55, (6, 5)),
+    # single elements and partial last element groups of the x-line kernels
+    # (16 / 8 / 4 elements per group for p = 1 / 2 / 3), other n_q instances
+    (3, 1, 2, O.MU_303, (1, 1, 1)), (3, 2, 3, O.MU_303, (1, 1, 1)), (3, 3, 4, O.MU_303, (1, 1, 1)),
+    (3, 4, 5, O.MU_303, (1, 1, 1)), (3, 1, 4, O.MU_303, (17, 3, 5)), (3, 2, 5, O.MU_303, (9, 7, 3)),
+    (3, 3, 6, O.MU_303, (5, 3, 7)), (3, 2, 4, O.MU_302, (9, 7, 3)), (3, 3, 5, O.MU_321, (5, 3, 7)),
 ])
 def test_operator_matches_oracle(dim, order, nq, metric, counts, rng):
     import paper_2205_12721_b200 as P
