@@ -297,6 +297,30 @@ def kershaw_paper_table(orders=(1, 2, 3, 4)):
     return out
 
 
+def c1_solve():
+    """BASELINE configs[0] (C1): 2D Q2 16x16 unit square, perturbed interior
+    (amp 0.2, seed 20240901), mu_2, n_q = 4, 5 Newton iterations, Jacobi-MINRES
+    -- the case the CPU reference runs in 2.85 s.
+    Wall time of the warm solve (second of two)."""
+    import torch
+
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(2, (16, 16), 2)
+    x0 = torch.from_numpy(perturbed_x(mesh)).cuda()
+    prob = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_2, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), 4)
+    out = None
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        res = P.newton_solve(x0, prob, P.NewtonConfig(max_iterations=5), P.MinresConfig())
+        torch.cuda.synchronize()
+        out = {"workload": "C1: 2D Q2 16x16, mu_2, n_q=4, 5 Newton", "n_dofs": mesh.n_dofs,
+               "solve_s": time.perf_counter() - t, "newton_iterations": res.trace.newton_iterations,
+               "minres_iterations": res.trace.minres_total, "f_final": prob.objective(res.x),
+               "reference_cpu_s_survey": 2.85}
+    return out
+
+
 def newton_iteration(prob, x):
     """One Newton iteration, paper protocol (MINRES fixed at 20 iterations,
     PAPER.md:1002-1004): setup + diagonal + MINRES + line search."""
@@ -550,6 +574,7 @@ def main():
     if "newton" in head:
         line["newton_iteration"] = head["newton"]
     line["c2_small"] = small_config_c2()
+    line["c1_solve"] = c1_solve()
     if not args.no_newton:
         line["kershaw_paper_table"] = kershaw_paper_table()
     if world == 1 and not args.no_cpu:
