@@ -573,6 +573,9 @@ def main():
     }
     if "newton" in head:
         line["newton_iteration"] = head["newton"]
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()   # the small-problem sections below run after the 1e8-DOF ones
     line["c2_small"] = small_config_c2()
     line["c1_solve"] = c1_solve()
     if not args.no_newton:

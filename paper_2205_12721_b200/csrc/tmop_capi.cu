@@ -420,6 +420,10 @@ int tmop_hessian_setup(tmop_ctx *c, const double *x, double *qdata, tmop_det_sta
   return TMOP_OK;
 }
 
+// Slab-overlapped paths only pay off for long applies (>= ~0.5 ms); below
+// this many elements the extra launches cost more than the hidden gather.
+static const int64_t OVERLAP_MIN_ELEMENTS = getenv("TMOP_OVERLAP_MIN") ? atoll(getenv("TMOP_OVERLAP_MIN")) : 262144;
+
 // Overlapped action on a verified lattice: z-slab element launches on the
 // context stream; after each, the E->L sum of the node planes that slab
 // completes (ascending element order per node, as the one-shot gather) runs
@@ -478,7 +482,7 @@ int tmop_hessian_apply(tmop_ctx *c, const double *qdata, const double *v, double
   if (!c || !qdata || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
   // (p <= 3: the x-line element kernel leaves register room for the gather's
   // CTAs; measured 4-5 % faster there, slower at p = 4)
-  if (c->lat_p > 0 && c->n1 <= 4 && !c->lim_on && c->ov_slabs > 1 && c->ne >= (int64_t)c->ov_slabs * 4096)
+  if (c->lat_p > 0 && c->n1 <= 4 && !c->lim_on && c->ov_slabs > 1 && c->ne >= OVERLAP_MIN_ELEMENTS)
     return apply_overlapped(c, qdata, v, y);
   int rc = tmop_hessian_apply_elements(c, qdata, v);
   if (rc) return rc;
@@ -679,7 +683,7 @@ int tmop_minres_step_op(tmop_ctx *c, const double *qdata, int64_t n, double *Av,
   if (!c || !qdata || !st2) return fail(TMOP_ERR_ARG, "NULL argument");
   if (n != c->nn * c->dim) return fail(TMOP_ERR_ARG, "vector length %lld != dim * n_nodes", (long long)n);
   tmop_minres_state *cur = st2 + (k & 1), *nxt = st2 + ((k + 1) & 1);
-  if (c->lat_p > 0 && c->n1 <= 4 && !c->lim_on && c->ov_slabs > 1 && c->ne >= (int64_t)c->ov_slabs * 4096) {
+  if (c->lat_p > 0 && c->n1 <= 4 && !c->lim_on && c->ov_slabs > 1 && c->ne >= OVERLAP_MIN_ELEMENTS) {
     // overlapped: element kernel by z-slab on the context stream, the fused
     // E->L + K1 of each finished node range on the second stream (its K1
     // partials in a per-slab block of vpart1), then K2 / K3 reduce them all
@@ -704,6 +708,7 @@ int tmop_minres_step_op(tmop_ctx *c, const double *qdata, int64_t n, double *Av,
         a.restr = c->restr + e0 * c->NP;
         a.E = c->E + e0 * c->dim * c->NP;
         a.ne = e1 - e0;
+        a.stop = &cur->done;
         rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
         if (rc) return rc;
       }
@@ -730,6 +735,7 @@ int tmop_minres_step_op(tmop_ctx *c, const double *qdata, int64_t n, double *Av,
   ElemArgs a = base_args(c);
   a.in = v;
   a.qdata = qdata;
+  a.stop = &cur->done;
   int rc = run(c, metric_is_template(c->metric) ? K_APPLY : K_APPLY_NT, a, nullptr);
   if (rc) return rc;
   if (c->lim_on) {

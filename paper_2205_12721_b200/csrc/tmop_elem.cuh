@@ -155,6 +155,7 @@ struct ElemArgs {
   double lim_delta;
   double lim_base;    // 2 * weight * det_w  (operator.py:477)
   int lim_mask;       // zero constrained input components (hessian_apply)
+  const int32_t *stop;   // if non-NULL and *stop != 0 the launch is a no-op (converged MINRES)
 };
 
 // Point slot of quadrature point q (x fastest, fe.py:134-140) inside a lean
@@ -595,6 +596,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
   __shared__ int64_t red_i[CF::NT / 32];
   __shared__ __align__(8) uint64_t qbar;
 
+  if (a.stop && *a.stop) return;
   double acc = 0.0;
   MinLoc mn{DBL_MAX, LLONG_MAX};
 

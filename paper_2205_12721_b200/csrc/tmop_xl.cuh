@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
   __shared__ double red_v[(RSUM || RMIN) ? NT : 1];
   __shared__ int64_t red_i[RMIN ? NT : 1];
 
+  if (a.stop && *a.stop) return;          // converged MINRES: the step is a no-op
   const int tid = threadIdx.x;
   const int e = tid % EPB;                // element slot of this thread (all stages)
   const int item = tid / EPB;

@@ -31,7 +31,9 @@ class MinresConfig:
     max_iterations: int = 50
     rel_tolerance: float = 1e-8
     preconditioned: bool = True
-    check_every: int = 1   # device state is read every k iterations (results identical for any k)
+    # device state is read every k iterations (results identical for any k:
+    # once converged every fused step -- element kernel included -- is a no-op)
+    check_every: int = 8
     # Replay the fused TMOP iteration as a CUDA graph of 6 iterations (the
     # buffer rotation and the state parity repeat with period 6).  None = auto
     # (small problems, where launch latency dominates).
@@ -237,7 +239,8 @@ def _minres_body(apply_op: Callable, b, cfg: MinresConfig, precond, ctx, operato
         return h
     k = 0
     done = False
-    use_graph = operator is not None and (cfg.graph if cfg.graph is not None else n <= 4_000_000)
+    # graphs only where launch latency dominates (each capture costs ~5-10 ms of host time)
+    use_graph = operator is not None and (cfg.graph if cfg.graph is not None else n <= 250_000)
     if use_graph and cfg.max_iterations >= 7:
         # one eager iteration (configures the kernels), then 6-iteration graphs
         bufs_r = [r1, r2, spare]

@@ -11,6 +11,10 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# the slab-overlapped apply / MINRES paths start at 256 K elements by default;
+# the tests exercise them on a 34 x 32 x 32 mesh (read once when the library loads)
+os.environ.setdefault("TMOP_OVERLAP_MIN", "32768")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")

@@ -7,6 +7,8 @@ Newton traces: alpha and MINRES iteration counts exact, F / |grad F| 1e-9,
 final x 1e-10 relative.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -442,6 +444,7 @@ def test_overlapped_apply_and_minres_match_one_shot(rng, monkeypatch):
     x = O.perturb(om, rng, 0.2)
     v = torch.from_numpy(rng.standard_normal(x.shape)).cuda()
     out = {}
+    assert os.environ.get("TMOP_OVERLAP_MIN") == "32768", "run with TMOP_OVERLAP_MIN=32768 (set in conftest)"
     for slabs in ("1", "8"):
         monkeypatch.setenv("TMOP_APPLY_SLABS", slabs)
         mesh = P.build_box(3, counts, 1)
