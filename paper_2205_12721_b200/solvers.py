@@ -35,8 +35,8 @@ class MinresConfig:
     # once converged every fused step -- element kernel included -- is a no-op)
     check_every: int = 8
     # Replay the fused TMOP iteration as a CUDA graph of 6 iterations (the
-    # buffer rotation and the state parity repeat with period 6).  None = auto
-    # (small problems, where launch latency dominates).
+    # buffer rotation and the state parity repeat with period 6).  None / False
+    # = eager launches.
     graph: bool | None = None
 
     def validate(self) -> None:
@@ -239,8 +239,11 @@ def _minres_body(apply_op: Callable, b, cfg: MinresConfig, precond, ctx, operato
         return h
     k = 0
     done = False
-    # graphs only where launch latency dominates (each capture costs ~5-10 ms of host time)
-    use_graph = operator is not None and (cfg.graph if cfg.graph is not None else n <= 250_000)
+    # CUDA-graph replay is opt-in: a capture costs 5-10 ms of host time per
+    # MINRES call, more than it saves on one 50-iteration solve (measured on C1
+    # and the Kershaw sizes); eager launches with a state read every
+    # `check_every` iterations are the default
+    use_graph = operator is not None and bool(cfg.graph)
     if use_graph and cfg.max_iterations >= 7:
         # one eager iteration (configures the kernels), then 6-iteration graphs
         bufs_r = [r1, r2, spare]
