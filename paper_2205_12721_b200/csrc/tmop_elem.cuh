@@ -659,7 +659,12 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
 
     // ---- point stage
     for (int w = threadIdx.x; w < EPB * QP; w += CF::NT) {
-      const int e = w / QP, q = w % QP;
+      // 3D, unswizzled lines: threads walk the lean record's slot order
+      // (qx slowest) -- unit-stride Q-data reads / setup writes and odd-stride
+      // (conflict-free) gradient-buffer accesses; otherwise point order
+      constexpr bool SLOTW = DIM == 3 && !CF::SWZ;
+      const int e = w / QP, r = w % QP;
+      const int q = SLOTW ? (r / (Q * Q)) + Q * (r % (Q * Q)) : r;
       const int64_t eg = e0 + e;
       if (eg >= a.ne) continue;
       const int gi = CF::gs(q / Q, q % Q);   // (padded / swizzled) slot of the point
