@@ -109,6 +109,16 @@ class SlabPartition:
         return slice(0, self.n_owned)
 
 
+def _staged(t, group):
+    """gloo moves host memory only: CUDA tensors go through a host copy when
+    the group's backend is gloo (the 2-process, 1-GPU tests); NCCL keeps
+    device tensors."""
+    import torch.distributed as dist
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        return t.cpu(), True
+    return t, False
+
+
 class HaloExchange:
     """Sum of the shared node planes with the z-neighbours (torch.distributed
     point-to-point, batched; NCCL on GPUs, gloo on CPUs)."""
@@ -129,13 +139,13 @@ class HaloExchange:
         ops, recv = [], []
         pl = pt.plane
         if pt.has_lower:
-            send_lo = y2[:, :pl].contiguous()
+            send_lo, _ = _staged(y2[:, :pl].contiguous(), self.group)
             recv_lo = torch.empty_like(send_lo)
             ops += [dist.P2POp(dist.isend, send_lo, pt.rank - 1, self.group),
                     dist.P2POp(dist.irecv, recv_lo, pt.rank - 1, self.group)]
             recv.append(("lo", recv_lo))
         if pt.has_upper:
-            send_hi = y2[:, pt.n_local - pl:].contiguous()
+            send_hi, _ = _staged(y2[:, pt.n_local - pl:].contiguous(), self.group)
             recv_hi = torch.empty_like(send_hi)
             ops += [dist.P2POp(dist.isend, send_hi, pt.rank + 1, self.group),
                     dist.P2POp(dist.irecv, recv_hi, pt.rank + 1, self.group)]
@@ -145,6 +155,7 @@ class HaloExchange:
         for r in dist.batch_isend_irecv(ops):
             r.wait()
         for side, buf in recv:
+            buf = buf.to(y.device, non_blocking=True)
             if side == "lo":
                 y2[:, :pl] += buf
             else:
@@ -193,7 +204,7 @@ class DistributedProblem:
         torch = _torch()
         import torch.distributed as dist
         dev = self.fixed2.device
-        t = torch.tensor([value], dtype=torch.float64, device=dev)
+        t, _ = _staged(torch.tensor([value], dtype=torch.float64, device=dev), self.group)
         dist.all_reduce(t, op=op, group=self.group)
         return float(t.item())
 
