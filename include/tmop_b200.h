@@ -146,6 +146,11 @@ int tmop_hessian_diagonal(tmop_ctx *ctx, const double *qdata, double *diag);
 /* AddMultPA: gradient (operator.py:328-346). */
 int tmop_gradient(tmop_ctx *ctx, const double *x, double *grad,
                   tmop_det_status *det_out);
+/* Gradient, energy and min det(A) from ONE element pass (the line search's
+ * trial evaluation, solvers.py:210-216): energy_out (device scalar, may be
+ * NULL) = objective(x) up to summation order. */
+int tmop_gradient_energy(tmop_ctx *ctx, const double *x, double *grad, double *energy_out,
+                         tmop_det_status *det_out);
 /* GetLocalStateEnergyPA: objective (operator.py:311-326).  Writes F (incl.
  * the limiting term when configured) to *energy_out (device). */
 int tmop_objective(tmop_ctx *ctx, const double *x, double *energy_out,

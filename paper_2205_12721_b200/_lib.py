@@ -62,6 +62,7 @@ _SIGS = {
     "tmop_hessian_apply_gather": [_P, _P, _P],
     "tmop_hessian_diagonal": [_P, _P, _P],
     "tmop_gradient": [_P, _P, _P, _P],
+    "tmop_gradient_energy": [_P, _P, _P, _P, _P],
     "tmop_objective": [_P, _P, _P, _P],
     "tmop_min_det": [_P, _P, _P],
     "tmop_element_min_det": [_P, _P, _P, _P],

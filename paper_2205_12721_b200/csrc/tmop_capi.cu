@@ -548,7 +548,15 @@ int tmop_hessian_diagonal(tmop_ctx *c, const double *qdata, double *diag) {
 }
 
 int tmop_gradient(tmop_ctx *c, const double *x, double *grad, tmop_det_status *det_out) {
+  return tmop_gradient_energy(c, x, grad, nullptr, det_out);
+}
+
+int tmop_gradient_energy(tmop_ctx *c, const double *x, double *grad, double *energy_out, tmop_det_status *det_out) {
   if (!c || !x || !grad || !det_out) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (energy_out && c->lim_on) {   // operator.py:324-325: the limiting value joins the energy
+    int rc0 = lim_value(c, x);
+    if (rc0) return rc0;
+  }
   ElemArgs a = base_args(c);
   a.in = x;
   int g = 0;
@@ -559,7 +567,8 @@ int tmop_gradient(tmop_ctx *c, const double *x, double *grad, tmop_det_status *d
     if (rc) return rc;
   }
   launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 1, nullptr, c->lim_on ? c->lim_y : nullptr, grad, c->stream);
-  launch_fin(g, nullptr, c->part_min, c->part_arg, 0.0, nullptr, 0.0, nullptr, det_out, c->stream);
+  launch_fin(g, energy_out ? c->part_sum : nullptr, c->part_min, c->part_arg, base_args(c).coef_e, energy_out, 1.0,
+             (energy_out && c->lim_on) ? c->lim_val : nullptr, det_out, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }

@@ -709,7 +709,8 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
             store_point<DIM>(qo, QP, T);
             qo[DIM * DIM * QP] = lean_k0(a.metric, a.coef_h * wpt, tau);
             qo[(DIM * DIM + 1) * QP] = 1.0 / tau;
-          } else {  // K_GRAD
+          } else {  // K_GRAD (+ the energy, for the fused line-search evaluation)
+            acc += wpt * metric_mu<DIM>(a.metric, tau, I1, S);
             const double cw = a.coef_g * wpt;
             double P[DIM][DIM];
             if (metric_is_template(a.metric)) {
@@ -777,7 +778,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
   }
 
   // ---- per-CTA deterministic partials
-  if constexpr (KIND == K_ENERGY || KIND == K_VOLUME) {
+  if constexpr (KIND == K_ENERGY || KIND == K_VOLUME || KIND == K_GRAD) {
     const double s = block_sum<CF::NT>(acc, red_v);
     if (threadIdx.x == 0) a.part_sum[blockIdx.x] = s;
   }

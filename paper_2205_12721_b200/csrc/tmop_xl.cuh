@@ -270,7 +270,8 @@ __device__ __forceinline__ void xl_point_x(const ElemArgs &a, const Tab &t, int6
         for (int j = 0; j < 3; ++j) qo[(i * 3 + j) * QP] = T[i][j];
       qo[9 * QP] = lean_k0(a.metric, a.coef_h * wpt, tau);
       qo[10 * QP] = 1.0 / tau;
-    } else {  // K_GRAD: P = cw (a_t T + a_s S) (operator.py:328-346)
+    } else {  // K_GRAD: P = cw (a_t T + a_s S) (operator.py:328-346), + the energy
+      if (eg < a.ne) acc += wpt * metric_mu<3>(a.metric, tau, I1, S);   // (line-search evaluation)
       const double cw = a.coef_g * wpt;
       double P[3][3];
       if (metric_is_template(a.metric)) {
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
   constexpr bool BACK = xl_backward<KIND>();
   constexpr bool MASK = APPLY;          // the apply zeroes constrained inputs (operator.py:409)
   constexpr bool NTM = KIND == K_APPLY_NT;
-  constexpr bool RSUM = KIND == K_ENERGY || KIND == K_VOLUME;
+  constexpr bool RSUM = KIND == K_ENERGY || KIND == K_VOLUME || KIND == K_GRAD;
   constexpr bool RMIN = KIND == K_SETUP || KIND == K_GRAD || KIND == K_ENERGY || KIND == K_MINDET;
   constexpr int EPB = XC::EPB, NP = XC::NP, QP = XC::QP, QS = XC::QS, NT = XC::NT;
   constexpr int U_QZ = XC::U_QZ, W_QY = XC::W_QY, W_QZ = XC::W_QZ;

@@ -391,6 +391,22 @@ class TmopProblem:
         self._raise_if_inverted(xt, md)
         return self._out(g, host, out)
 
+    def evaluate_trial(self, x):
+        """(min det A, F, grad F) at a line-search trial point from ONE element
+        pass (tmop_gradient_energy) instead of three (solvers.py:210-216).
+        F and grad F are None when the mesh is inverted there -- the
+        reference evaluates neither in that case -- so nothing is raised."""
+        torch = _torch()
+        xt, host = self._in(x)
+        g = torch.empty_like(xt)
+        _lib.check(self.lib.tmop_gradient_energy(self._ctx, _lib.ptr(xt), _lib.ptr(g), _lib.ptr(self._scalar),
+                                                 _lib.ptr(self._status)), "tmop_gradient_energy")
+        self._count("gradient")
+        md, _ = self._det()
+        if not md > 0.0:
+            return md, None, None
+        return md, float(self._scalar.item()), self._out(g, host)
+
     def hessian_setup(self, x) -> HessQData:
         torch = _torch()
         xt, host = self._in(x)

@@ -375,9 +375,22 @@ def line_search(x, dx, problem: ProblemLike, f0: float, grad_norm0: float, max_h
         raise LineSearchError("step direction contains non-finite entries")
     alpha = 1.0
     xt = torch.empty_like(xd)
+    fused = getattr(problem, "evaluate_trial", None)
     for _ in range(max_halvings + 1):
         _lib.check(lib.tmop_trial_point(ctx, xd.numel(), _lib.ptr(xd), _lib.ptr(dxd), alpha, _lib.ptr(xt)),
                    "tmop_trial_point")
+        if fused is not None:
+            # one element pass gives min det, F and grad F; same acceptance tests
+            md, ft, gt = fused(xt)
+            if md > 0.0 and ft < GROWTH_FACTOR * f0:
+                gtd, _ = _dev(gt, xd.device)
+                ngt = _norm(ctx, gtd, scratch)
+                if ngt < GROWTH_FACTOR * grad_norm0:
+                    if host:
+                        return LineSearchResult(alpha, xt.cpu().numpy(), ft, ngt, md, gtd.cpu().numpy())
+                    return LineSearchResult(alpha, xt, ft, ngt, md, gtd)
+            alpha *= 0.5
+            continue
         md = problem.min_det_jacobian(xt)
         if md > 0.0:
             ft = problem.objective(xt)
