@@ -302,7 +302,7 @@ __device__ __forceinline__ void f2_3d(const Tab &t, const double *R2, double *R1
 template <int N, int Q, int C>
 __device__ __forceinline__ void f3_3d(const Tab &t, const double *R1, double *R2) {
   using CF = Cfg<3, N, Q>;
-  constexpr int ITEMS = C * Q * Q, QP = Q * Q * Q;
+  constexpr int ITEMS = C * Q * Q;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * Q), qq = r % (Q * Q);
     constexpr int WF = CF::WF, GF = CF::GF;
@@ -337,7 +337,7 @@ __device__ __forceinline__ void f3_3d(const Tab &t, const double *R1, double *R2
 template <int N, int Q>
 __device__ __forceinline__ void b3_3d(const Tab &t, const double *R2, double *R1) {
   using CF = Cfg<3, N, Q>;
-  constexpr int ITEMS = 3 * Q * Q, QP = Q * Q * Q;
+  constexpr int ITEMS = 3 * Q * Q;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * Q), qq = r % (Q * Q);
     constexpr int WF = CF::WF, GF = CF::GF;
@@ -454,7 +454,7 @@ __device__ __forceinline__ void f1_2d(const Tab &t, const double *R1, double *R2
 template <int N, int Q, int C>
 __device__ __forceinline__ void f2_2d(const Tab &t, const double *R2, double *G) {
   using CF = Cfg<2, N, Q>;
-  constexpr int ITEMS = C * Q, QP = Q * Q;
+  constexpr int ITEMS = C * Q;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / Q, qy = r % Q;
     constexpr int NL = CF::NL, GF = CF::GF;
@@ -483,7 +483,7 @@ __device__ __forceinline__ void f2_2d(const Tab &t, const double *R2, double *G)
 template <int N, int Q>
 __device__ __forceinline__ void b2_2d(const Tab &t, const double *Z, double *R2) {
   using CF = Cfg<2, N, Q>;
-  constexpr int ITEMS = 2 * Q, QP = Q * Q;
+  constexpr int ITEMS = 2 * Q;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / Q, qy = r % Q;
     constexpr int NL = CF::NL, GF = CF::GF;
