@@ -559,6 +559,7 @@ int tmop_gradient_energy(tmop_ctx *c, const double *x, double *grad, double *ene
   }
   ElemArgs a = base_args(c);
   a.in = x;
+  a.energy = energy_out != nullptr;
   int g = 0;
   int rc = run(c, K_GRAD, a, &g);
   if (rc) return rc;

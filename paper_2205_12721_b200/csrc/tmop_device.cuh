@@ -135,7 +135,7 @@ __device__ __forceinline__ double metric_mu(int metric, double tau, double I1, c
   switch (metric) {
     case MU2: return I1 / (2.0 * tau) - 1.0;
     case MU55: { double t = tau - 1.0; return t * t; }
-    case MU303: return I1 / (3.0 * cbrt(tau * tau)) - 1.0;
+    case MU303: return I1 * rcbrt(tau * tau) * (1.0 / 3.0) - 1.0;
     case MU7: return I1 + mfro2<D>(S) - 2.0 * D;
     case MU302: return I1 * mfro2<D>(S) / 9.0 - 1.0;
     default: /* MU321 */ return I1 + mfro2<D>(S) - 2.0 * D;
@@ -149,9 +149,25 @@ __device__ __forceinline__ void metric_first_coeffs(int metric, double tau, doub
     case MU55: at = 0.0; as = 2.0 * tau * (tau - 1.0); break;
     case MU7: { double it2 = 1.0 / (tau * tau); at = 2.0 * (1.0 + it2); as = -2.0 * I1 * it2; } break;
     default: /* MU303 */ {
-      double r = 1.0 / cbrt(tau * tau);
+      double r = rcbrt(tau * tau);
       at = (2.0 / 3.0) * r; as = -(2.0 / 9.0) * I1 * r;
     }
+  }
+}
+
+// mu (when `want_mu`) and (a_t, a_s) of a template metric from one rcbrt:
+// bitwise the values metric_mu / metric_first_coeffs return (the gradient
+// kernel's fused line-search energy, solvers.py:210-216).
+template <int D>
+__device__ __forceinline__ void metric_mu_first(int metric, double tau, double I1, const double (&S)[D][D],
+                                                bool want_mu, double &mu, double &at, double &as) {
+  if (metric == MU303) {
+    const double r = rcbrt(tau * tau);
+    if (want_mu) mu = I1 * r * (1.0 / 3.0) - 1.0;
+    at = (2.0 / 3.0) * r; as = -(2.0 / 9.0) * I1 * r;
+  } else {
+    if (want_mu) mu = metric_mu<D>(metric, tau, I1, S);
+    metric_first_coeffs(metric, tau, I1, at, as);
   }
 }
 
@@ -164,7 +180,7 @@ __device__ __forceinline__ void metric_second_coeffs(int metric, double tau, dou
     case MU7: { double it2 = 1.0 / (tau * tau);
       c[0] = 2.0 * (1.0 + it2); c[1] = -4.0 * it2; c[2] = 4.0 * I1 * it2; c[3] = 2.0 * I1 * it2; } break;
     default: /* MU303 */ {
-      double r = 1.0 / cbrt(tau * tau);
+      double r = rcbrt(tau * tau);
       c[0] = (2.0 / 3.0) * r; c[1] = -(4.0 / 9.0) * r;
       c[2] = (4.0 / 27.0) * I1 * r; c[3] = (2.0 / 9.0) * I1 * r;
     }
@@ -183,7 +199,7 @@ __device__ __forceinline__ void metric_second_coeffs(int metric, double tau, dou
 //   mu_302 / mu_321: k0 = sw (non-template action, nt_hess)
 __device__ __forceinline__ double lean_k0(int metric, double sw, double tau) {
   switch (metric) {
-    case MU303: return sw * (1.0 / cbrt(tau * tau));
+    case MU303: return sw * rcbrt(tau * tau);
     case MU2: return sw / tau;
     default: return sw;
   }

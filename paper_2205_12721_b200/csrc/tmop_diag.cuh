@@ -75,10 +75,31 @@ __global__ void __launch_bounds__(ELEM_NT) diag2_kernel(const ElemArgs a, const 
   double *RA = smem;
   double *RB = RA + EPB * DC::RA;
 
+  // Lean point records of the NEXT group are loaded into registers while the
+  // current group runs its sweeps (one or two points per thread), so the
+  // point stage never waits on DRAM latency.
+  constexpr int PTS = (EPB * QP + ELEM_NT - 1) / ELEM_NT, LW = DIM * DIM + 2;
+  double qn[PTS][LW];
+  auto fetch = [&](int64_t g) {
+#pragma unroll
+    for (int j = 0; j < PTS; ++j) {
+      const int w = threadIdx.x + j * ELEM_NT;
+      const int64_t eg = g * EPB + w / QP;
+      if (w < EPB * QP && g < a.ngroups && eg < a.ne) {
+        const double *q = a.qdata + eg * QS + w % QP;
+#pragma unroll
+        for (int k = 0; k < LW; ++k) qn[j][k] = __ldg(q + k * QP);
+      }
+    }
+  };
+  fetch(blockIdx.x);
   for (int64_t grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
     const int64_t e0 = grp * EPB;
     // ---- point stage: Hpair[c*NPAIR + f][slot]
-    for (int w = threadIdx.x; w < EPB * QP; w += ELEM_NT) {
+#pragma unroll
+    for (int j = 0; j < PTS; ++j) {
+      const int w = threadIdx.x + j * ELEM_NT;
+      if (w >= EPB * QP) break;
       const int e = w / QP, slot = w % QP;
       const int64_t eg = e0 + e;
       double *hp = RA + e * DC::RA + slot;
@@ -87,8 +108,16 @@ __global__ void __launch_bounds__(ELEM_NT) diag2_kernel(const ElemArgs a, const 
         for (int f = 0; f < NF; ++f) hp[f * QP] = 0.0;
         continue;
       }
-      double T[DIM][DIM], S[DIM][DIM], k0, itau;
-      lean_load<DIM>(a.qdata + eg * QS + slot, QP, T, S, k0, itau);
+      double T[DIM][DIM], S[DIM][DIM], C[DIM][DIM], k0 = qn[j][DIM * DIM], itau = qn[j][DIM * DIM + 1];
+#pragma unroll
+      for (int r = 0; r < DIM; ++r)
+#pragma unroll
+        for (int cc = 0; cc < DIM; ++cc) T[r][cc] = qn[j][r * DIM + cc];
+      mcof<DIM>(T, C);
+#pragma unroll
+      for (int r = 0; r < DIM; ++r)
+#pragma unroll
+        for (int cc = 0; cc < DIM; ++cc) S[r][cc] = C[r][cc] * itau;
       if constexpr (!NTM) {
         double c[4];
         lean_coeffs(a.metric, k0, itau, mfro2<DIM>(T), c);
@@ -123,6 +152,7 @@ __global__ void __launch_bounds__(ELEM_NT) diag2_kernel(const ElemArgs a, const 
       }
     }
     __syncthreads();
+    fetch(grp + gridDim.x);
     // ---- x^T: RA [c*NPAIR+f][slot] -> RB [c*NPAIR+f][line][kx]
     for (int w = threadIdx.x; w < EPB * DIM * XL; w += ELEM_NT) {
       const int e = w / (DIM * XL), r = w % (DIM * XL), c = r / XL, line = r % XL;

@@ -155,6 +155,7 @@ struct ElemArgs {
   double lim_delta;
   double lim_base;    // 2 * weight * det_w  (operator.py:477)
   int lim_mask;       // zero constrained input components (hessian_apply)
+  int energy;         // K_GRAD: also accumulate the energy into part_sum
   const int32_t *stop;   // if non-NULL and *stop != 0 the launch is a no-op (converged MINRES)
 };
 
@@ -689,7 +690,8 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
         if constexpr (KIND == K_SETUP || KIND == K_GRAD || KIND == K_ENERGY) {
           const double tau = dj * a.inv_s_d;
           const double I1 = mfro2<DIM>(A) * (a.inv_s * a.inv_s);
-          const double cs = a.inv_s_dm1 / tau;
+          const double itau = 1.0 / tau;   // the one division of the point
+          const double cs = a.inv_s_dm1 * itau;
           double Cof[DIM][DIM];
           mcof<DIM>(A, Cof);
           double S[DIM][DIM], T[DIM][DIM];
@@ -708,21 +710,22 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
             double *qo = a.qout + eg * QS + lean_slot<DIM, Q>(q);
             store_point<DIM>(qo, QP, T);
             qo[DIM * DIM * QP] = lean_k0(a.metric, a.coef_h * wpt, tau);
-            qo[(DIM * DIM + 1) * QP] = 1.0 / tau;
+            qo[(DIM * DIM + 1) * QP] = itau;
           } else {  // K_GRAD (+ the energy, for the fused line-search evaluation)
-            acc += wpt * metric_mu<DIM>(a.metric, tau, I1, S);
             const double cw = a.coef_g * wpt;
             double P[DIM][DIM];
             if (metric_is_template(a.metric)) {
-              double at, as;
-              metric_first_coeffs(a.metric, tau, I1, at, as);
+              double at, as, mu = 0.0;
+              metric_mu_first<DIM>(a.metric, tau, I1, S, a.energy, mu, at, as);
+              if (a.energy) acc += wpt * mu;
               const double ct = cw * at * a.inv_s;
-              const double cc = cw * as * a.inv_s_dm1 / tau;
+              const double cc = cw * as * a.inv_s_dm1 * itau;
 #pragma unroll
               for (int i = 0; i < DIM; ++i)
 #pragma unroll
                 for (int j = 0; j < DIM; ++j) P[i][j] = ct * A[i][j] + cc * Cof[i][j];
             } else {
+              if (a.energy) acc += wpt * metric_mu<DIM>(a.metric, tau, I1, S);
               nt_first<DIM>(a.metric, T, S, P);
 #pragma unroll
               for (int i = 0; i < DIM; ++i)
