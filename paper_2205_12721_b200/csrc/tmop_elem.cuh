@@ -52,6 +52,12 @@ enum Kind : int {
 #ifndef TMOP_SMEM_BUDGET
 #define TMOP_SMEM_BUDGET 0
 #endif
+#ifndef TMOP_WIDE_LDG
+#define TMOP_WIDE_LDG 1
+#endif
+#ifndef TMOP_WIDE_MINB
+#define TMOP_WIDE_MINB 2
+#endif
 #ifndef TMOP_MIN_BLOCKS
 #define TMOP_MIN_BLOCKS 0
 #endif
@@ -60,6 +66,7 @@ constexpr int ELEM_NT = 256;   // diagonal kernel
 
 __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 __host__ __device__ constexpr int cclamp(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // Element-group size of the 3D x-line kernels (tmop_xl.cuh): 16 elements per
@@ -119,13 +126,27 @@ struct Cfg {
   // CTA's shared memory; measured 1.4-1.8x faster at n_q = 9, round 1)
   static constexpr bool WIDE = Q >= 7;
   static constexpr int NT = TMOP_ELEM_NT ? TMOP_ELEM_NT : (WIDE ? 256 : 128);
-  static constexpr int MINB = TMOP_MIN_BLOCKS ? TMOP_MIN_BLOCKS : (WIDE ? 1 : 4);
+  // n_q >= 7 Hessian action: the point stage reads its Q-data straight from
+  // HBM (unit stride in slot order) instead of staging a 64 KB element block,
+  // which halves the CTA's shared memory and doubles the resident CTAs
+  static constexpr bool QLDG = WIDE && TMOP_WIDE_LDG;
+  static constexpr int MINB = TMOP_MIN_BLOCKS ? TMOP_MIN_BLOCKS : (WIDE ? (QLDG ? TMOP_WIDE_MINB : 1) : 4);
+  // n_q >= 7: the work arrays (~70-82 KB) allow 2-3 CTAs / SM; the register
+  // target follows (the forward-only kinds need ~80 registers)
+  template <int KIND>
+  static constexpr int minb() {
+    return (!WIDE || TMOP_MIN_BLOCKS) ? MINB
+           : KIND == K_APPLY ? MINB
+           : KIND == K_APPLY_NT ? 1
+           : (KIND == K_SETUP || KIND == K_GRAD || KIND == K_DIAG || KIND == K_DIAG_NT) ? 2
+           : cmin(3, (227 * 1024) / (EPB * PER * 8 + 1024));
+  }
   static constexpr int BUDGET = TMOP_SMEM_BUDGET ? TMOP_SMEM_BUDGET : (WIDE ? 9216 : 7168);
   // elements per CTA: work arrays + staged Q-data within BUDGET doubles
-  static constexpr int EPB = cclamp(BUDGET / (PER + QS), 1, 32);
+  static constexpr int EPB = cclamp(BUDGET / (PER + (QLDG ? 0 : QS)), 1, 32);
   static constexpr int QOFF = (EPB * PER + 1) & ~1;          // Q-data staging offset (doubles)
   static constexpr int SMEM = EPB * PER * 8;                 // kernels without staging
-  static constexpr int SMEM_TMA = (QOFF + EPB * QS) * 8;     // Hessian-action kernels
+  static constexpr int SMEM_TMA = QLDG ? SMEM : (QOFF + EPB * QS) * 8;   // Hessian-action kernels
 };
 
 struct ElemArgs {
@@ -585,10 +606,11 @@ __device__ __forceinline__ void lean_hess(int metric, const double *qd, int QP, 
 
 // ------------------------------------------------------ the kernel
 template <int DIM, int N, int Q, int KIND>
-__global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
+__global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::template minb<KIND>()) elem_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
   using CF = Cfg<DIM, N, Q>;
   constexpr int QP = CF::QP, EPB = CF::EPB, QS = CF::QS;
   constexpr bool APPLY = (KIND == K_APPLY || KIND == K_APPLY_NT);
+  constexpr bool STAGE = APPLY && !CF::QLDG;   // Q-data staged in shared memory by TMA
   extern __shared__ __align__(16) double smem[];
   double *R1 = smem;
   double *R2 = smem + EPB * CF::R1;
@@ -613,7 +635,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
     tma_load_1d(QB, a.qdata + e0 * QS, bytes, &qbar);
   };
   uint32_t phase = 0;
-  if constexpr (APPLY) {
+  if constexpr (STAGE) {
     if (threadIdx.x == 0) {
       mbar_init(&qbar, 1);
       mbar_fence_init();
@@ -631,6 +653,15 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
 
   for (int64_t grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
     const int64_t e0 = grp * EPB;
+    if constexpr (APPLY && CF::QLDG) {
+      // the next group's Q-data block -> L2 while this group runs, so the
+      // point stage's direct loads of it hit L2
+      const int64_t nxt = grp + gridDim.x;
+      if (threadIdx.x == 0 && nxt < a.ngroups) {
+        const int64_t cnt = (a.ne - nxt * EPB) < EPB ? (a.ne - nxt * EPB) : EPB;
+        l2_prefetch_bulk(a.qdata + nxt * EPB * QS, (uint32_t)(cnt * QS * 8));
+      }
+    }
     if constexpr (APPLY) {
       pre.store(R1);
     } else {
@@ -655,7 +686,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
       Gp = R1;
       gstride = CF::R1;
     }
-    if constexpr (APPLY) mbar_wait(&qbar, phase);
+    if constexpr (STAGE) mbar_wait(&qbar, phase);
     __syncthreads();
 
     // ---- point stage
@@ -675,7 +706,8 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
 
       if constexpr (APPLY) {
         double z[DIM][DIM];
-        lean_hess<DIM, KIND == K_APPLY_NT>(a.metric, QB + e * QS + lean_slot<DIM, Q>(q), QP, A, z);
+        const double *qp = (CF::QLDG ? a.qdata + eg * QS : QB + e * QS) + lean_slot<DIM, Q>(q);
+        lean_hess<DIM, KIND == K_APPLY_NT>(a.metric, qp, QP, A, z);
         store_point<DIM>(gp, CF::GF, z);
       } else {
         // A is the Jacobian dx/dxi at the point
@@ -742,7 +774,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::MINB) elem
       // the staging buffer is free again: stream in the next group's Q-data
       phase ^= 1u;
       const int64_t nxt = grp + gridDim.x;
-      if (threadIdx.x == 0 && nxt < a.ngroups) issue(nxt);
+      if (STAGE && threadIdx.x == 0 && nxt < a.ngroups) issue(nxt);
       pre.load_values(a);                              // group nxt (indices loaded last iteration)
       pre.load_index(a, (nxt + gridDim.x) * EPB);       // group after nxt
     }
