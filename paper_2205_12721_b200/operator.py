@@ -451,7 +451,8 @@ class TmopProblem:
     # slab k-1 run on three streams (PCIe is full duplex), so the end-to-end
     # time approaches max(H2D, D2H, compute) instead of their sum.  Bitwise
     # identical to the one-shot apply.
-    pipeline_slabs = int(os.environ.get("TMOP_PIPE_SLABS", "8"))
+    pipeline_slabs = int(os.environ.get("TMOP_PIPE_SLABS", "16"))
+    pipeline_ramp = os.environ.get("TMOP_PIPE_RAMP", "1") != "0"
 
     def _apply_host_pipelined(self, qdata: HessQData, vh, out):
         torch = _torch()
@@ -482,8 +483,16 @@ class TmopProblem:
             ex, ey, ez = e % nx, (e // nx) % ny, e // layer
             return (ex * p + p) + NX * ((ey * p + p) + NY * (ez * p + p)) + 1
 
+        # slab sizes ramp up and down (1/4, 1/2, 1, ..., 1, 1/2, 1/4): the
+        # first H2D and the last D2H are not overlapped, so they are kept short
         ns = min(self.pipeline_slabs, nz)
-        bounds = [((k * nz) // ns) * layer // 16 * 16 for k in range(ns)] + [ne]
+        w = [1.0] * ns
+        if self.pipeline_ramp and ns >= 8:
+            w[0] = w[-1] = 0.25
+            w[1] = w[-2] = 0.5
+        cum = np.concatenate([[0.0], np.cumsum(w)]) / sum(w)
+        zs = sorted(set(int(round(c * nz)) for c in cum[:-1]))
+        bounds = [z * layer // 16 * 16 for z in zs] + [ne]
         copied, done = 0, 0
         for k in range(ns):
             e0, e1 = bounds[k], bounds[k + 1]
