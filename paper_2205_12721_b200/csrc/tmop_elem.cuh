@@ -23,6 +23,7 @@
 #include <climits>
 
 #include "tmop_device.cuh"
+#include "tmop_elem_pad.h"
 
 namespace tmop {
 
@@ -107,13 +108,17 @@ struct Cfg {
       return l * QL + x;
     }
   }
-  static constexpr int WF = Q * Q * NL;                       // one (c, variant) block of W / A (3D)
+  static constexpr int WF = Q * Q * NL;                       // one (c, variant) block of W / A (2D layout)
+  // 3D sweep buffers (strides from tools/elem_banks.py, tmop_elem_pad.h)
+  using PAD = ElemPad<N, Q>;
+  static constexpr int UZ = PAD::UZ, UV = PAD::UV, UC = PAD::UC;
+  static constexpr int WY = PAD::WY, WZ = PAD::WZ, WV = PAD::WV, WC = PAD::WC;
   static constexpr int GF = DIM == 3 ? Q * Q * QL : Q * QL;   // one field of grad / z
   // 3D: R1 holds X / W / A (and det scratch); R2 holds U / grad+z / Bv.
   // 2D: R1 holds X / grad+z (and diag x-sweep); R2 holds U / A (and diag points).
   static constexpr int R1 =
-      DIM == 3 ? cmax(cmax(3 * NP, 9 * WF), QP) : cmax(cmax(2 * NP, 4 * GF), 2 * Q * N);
-  static constexpr int R2 = DIM == 3 ? cmax(6 * Q * N * N, 9 * GF) : cmax(4 * Q * NL, 2 * QP);
+      DIM == 3 ? cmax(cmax(3 * NP, 2 * WC + 3 * WV), cmax(QP, GF)) : cmax(cmax(2 * NP, 4 * GF), 2 * Q * N);
+  static constexpr int R2 = DIM == 3 ? cmax(2 * UC + 2 * UV, 9 * GF) : cmax(4 * Q * NL, 2 * QP);
   static constexpr int PER = R1 + R2;
   // lean Q-data: T (d*d), k0, itau per point; element stride rounded to an
   // even number of doubles so every element block is 16-byte aligned (TMA).
@@ -275,7 +280,7 @@ __device__ __forceinline__ void f1_3d(const Tab &t, const double *R1, double *R2
     double xv[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) xv[k] = x[k * N * N];
-    double *u = R2 + e * CF::R2 + c * 2 * Q * N * N + kk;
+    double *u = R2 + e * CF::R2 + c * CF::UC + kk;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       double sb = 0.0, sg = 0.0;
@@ -284,8 +289,8 @@ __device__ __forceinline__ void f1_3d(const Tab &t, const double *R1, double *R2
         sb += tB<Q, N>(t, q, k) * xv[k];
         sg += tG<Q, N>(t, q, k) * xv[k];
       }
-      u[q * N * N] = sb;
-      u[Q * N * N + q * N * N] = sg;
+      u[q * CF::UZ] = sb;
+      u[CF::UV + q * CF::UZ] = sg;
     }
   }
 }
@@ -297,13 +302,13 @@ __device__ __forceinline__ void f2_3d(const Tab &t, const double *R2, double *R1
   constexpr int ITEMS = C * Q * N;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * N), r2 = r % (Q * N), qz = r2 / N, kx = r2 % N;
-    const double *ub = R2 + e * CF::R2 + (c * 2 + 0) * Q * N * N + qz * N * N + kx;
-    const double *ug = ub + Q * N * N;
+    const double *ub = R2 + e * CF::R2 + c * CF::UC + qz * CF::UZ + kx;
+    const double *ug = ub + CF::UV;
     double vb[N], vg[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) { vb[k] = ub[k * N]; vg[k] = ug[k * N]; }
-    constexpr int NL = CF::NL, WF = CF::WF;
-    double *wb = R1 + e * CF::R1 + (c * 3) * WF + qz * Q * NL + kx;
+    constexpr int NL = CF::WY, WF = CF::WV;
+    double *wb = R1 + e * CF::R1 + c * CF::WC + qz * CF::WZ + kx;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -327,8 +332,8 @@ __device__ __forceinline__ void f3_3d(const Tab &t, const double *R1, double *R2
   constexpr int ITEMS = C * Q * Q;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * Q), qq = r % (Q * Q);
-    constexpr int WF = CF::WF, GF = CF::GF;
-    const double *wb = R1 + e * CF::R1 + (c * 3) * WF + qq * CF::NL;
+    constexpr int WF = CF::WV, GF = CF::GF;
+    const double *wb = R1 + e * CF::R1 + c * CF::WC + (qq / Q) * CF::WZ + (qq % Q) * CF::WY;
     double bb[N], bg[N], gb[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -362,7 +367,7 @@ __device__ __forceinline__ void b3_3d(const Tab &t, const double *R2, double *R1
   constexpr int ITEMS = 3 * Q * Q;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * Q), qq = r % (Q * Q);
-    constexpr int WF = CF::WF, GF = CF::GF;
+    constexpr int WF = CF::WV, GF = CF::GF;
     const double *z = R2 + e * CF::R2 + (c * 3) * GF;
     double z0[Q], z1[Q], z2[Q];
 #pragma unroll
@@ -372,7 +377,7 @@ __device__ __forceinline__ void b3_3d(const Tab &t, const double *R2, double *R1
       z1[q] = z[GF + o];
       z2[q] = z[2 * GF + o];
     }
-    double *A = R1 + e * CF::R1 + (c * 3) * WF + qq * CF::NL;
+    double *A = R1 + e * CF::R1 + c * CF::WC + (qq / Q) * CF::WZ + (qq % Q) * CF::WY;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -396,8 +401,8 @@ __device__ __forceinline__ void b2_3d(const Tab &t, const double *R1, double *R2
   constexpr int ITEMS = 3 * Q * N;
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (Q * N), r2 = r % (Q * N), qz = r2 / N, kx = r2 % N;
-    constexpr int NL = CF::NL, WF = CF::WF;
-    const double *A = R1 + e * CF::R1 + (c * 3) * WF + qz * Q * NL + kx;
+    constexpr int NL = CF::WY, WF = CF::WV;
+    const double *A = R1 + e * CF::R1 + c * CF::WC + qz * CF::WZ + kx;
     double a0[Q], a1[Q], a2[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -405,7 +410,7 @@ __device__ __forceinline__ void b2_3d(const Tab &t, const double *R1, double *R2
       a1[q] = A[WF + q * NL];
       a2[q] = A[2 * WF + q * NL];
     }
-    double *b = R2 + e * CF::R2 + (c * 2) * Q * N * N + qz * N * N + kx;
+    double *b = R2 + e * CF::R2 + c * CF::UC + qz * CF::UZ + kx;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       double s0 = 0.0, s1 = 0.0;
@@ -415,7 +420,7 @@ __device__ __forceinline__ void b2_3d(const Tab &t, const double *R1, double *R2
         s1 += tB<Q, N>(t, q, k) * a2[q];
       }
       b[k * N] = s0;
-      b[Q * N * N + k * N] = s1;
+      b[CF::UV + k * N] = s1;
     }
   }
 }
@@ -429,10 +434,10 @@ __device__ __forceinline__ void b1_3d(const Tab &t, const double *R2, double *__
   for (int w = threadIdx.x; w < CF::EPB * ITEMS; w += CF::NT) {
     const int e = w / ITEMS, r = w % ITEMS, c = r / (N * N), kk = r % (N * N);
     if (e0 + e >= ne) continue;
-    const double *b = R2 + e * CF::R2 + (c * 2) * Q * N * N + kk;
+    const double *b = R2 + e * CF::R2 + c * CF::UC + kk;
     double b0[Q], b1[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) { b0[q] = b[q * N * N]; b1[q] = b[Q * N * N + q * N * N]; }
+    for (int q = 0; q < Q; ++q) { b0[q] = b[q * CF::UZ]; b1[q] = b[CF::UV + q * CF::UZ]; }
     double *out = E + ((e0 + e) * 3 + c) * NP + kk;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
