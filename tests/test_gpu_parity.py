@@ -120,6 +120,28 @@ def test_operator_matches_oracle(dim, order, nq, metric, counts, rng):
     assert p.min_det_jacobian(x) == pytest.approx(op.min_det_jacobian(x), rel=1e-14)
 
 
+@pytest.mark.parametrize("order,nq", [(o, q) for o in (1, 2, 3, 4) for q in (6, 7, 8, 9)])
+def test_padded_work_item_layouts_match_oracle(order, nq, rng):
+    """Every (n1, n_q) with per-configuration sweep-buffer strides
+    (tmop_elem_pad.h) and the direct-load n_q >= 7 Hessian action, against
+    the oracle: action, residual, energy, diagonal; mu_302 exercises the
+    non-template action."""
+    import paper_2205_12721_b200 as P
+    counts = (2, 2, 1) if order >= 3 else (3, 2, 2)
+    mesh = P.build_box(3, counts, order)
+    om = O.box_mesh(3, counts, order)
+    x = O.perturb(om, rng, 0.2)
+    v = rng.standard_normal(x.shape)
+    for metric in (O.MU_303, O.MU_302):
+        op = O.OracleProblem(om, metric, nq)
+        p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId(metric), P.TargetSpec(P.TargetKind.IDEAL_UNIT)), nq)
+        qd, oqd = p.hessian_setup(x), op.hessian_setup(x)
+        assert rel(p.hessian_apply(qd, v), op.hessian_apply(oqd, v)) <= TOL
+        assert rel(p.gradient(x), op.gradient(x)) <= TOL
+        assert p.objective(x) == pytest.approx(op.objective(x), rel=TOL)
+        assert rel(p.hessian_diagonal(qd), op.hessian_diagonal(oqd)) <= TOL
+
+
 def test_metric_points_match_reference():
     import paper_2205_12721_b200 as P
     g = load_golden("metric_points")
