@@ -132,6 +132,13 @@ class HaloExchange:
     def sum_planes(self, y):
         """y: local T-vector (3 * n_local); the bottom / top planes receive the
         neighbour's partial sums (in place)."""
+        return self.finish(y, self.start(y))
+
+    def start(self, y):
+        """Post the plane exchange of y's outer node planes (send copies,
+        receive buffers); with NCCL the transfer runs on NCCL's stream after
+        the work already queued on the current stream, so kernels queued
+        after this call overlap it."""
         torch = _torch()
         import torch.distributed as dist
         pt = self.part
@@ -151,8 +158,19 @@ class HaloExchange:
                     dist.P2POp(dist.irecv, recv_hi, pt.rank + 1, self.group)]
             recv.append(("hi", recv_hi))
         if not ops:
+            return None
+        return dist.batch_isend_irecv(ops), recv
+
+    def finish(self, y, pending):
+        """Wait for the exchange posted by start() and add the neighbours'
+        partial sums into y's planes."""
+        if pending is None:
             return y
-        for r in dist.batch_isend_irecv(ops):
+        pt = self.part
+        y2 = y.view(3, pt.n_local)
+        pl = pt.plane
+        works, recv = pending
+        for r in works:
             r.wait()
         for side, buf in recv:
             buf = buf.to(y.device, non_blocking=True)
@@ -195,6 +213,14 @@ class DistributedProblem:
         self.part = part
         self.group = group
         self.halo = HaloExchange(part, group)
+        # boundary-first Hessian action (outer layers + planes first, exchange
+        # overlapping the interior, whose E->L runs behind its element slabs
+        # on a second stream).  Off by default: at one rank it measures equal
+        # to the one-shot local action within run-to-run noise (7.3-7.7 ms
+        # either way, p=2 160^3) and the NVLink plane sum it would hide costs
+        # microseconds; for slower links set overlap = True (bitwise-identical
+        # result, tests/test_gpu_distributed.py).
+        self.overlap = False
         self.fixed2 = torch.as_tensor(np.ascontiguousarray(fixed_mask)).reshape(3, part.n_local)
         # adapters between torch tensors and the local operator's currency
         self._to = to_local or (lambda t: t)
@@ -229,8 +255,15 @@ class DistributedProblem:
         return self.local.hessian_setup(self._to(x))
 
     def hessian_apply(self, qdata, v):
-        y = self._from(self.local.hessian_apply(qdata, self._to(v)))
-        self.halo.sum_planes(y)
+        split = getattr(self.local, "hessian_apply_boundary_first", None)
+        if split is not None and self.overlap:
+            # outer layers first, plane exchange overlapping the interior
+            y, pending = split(qdata, self._to(v), self.halo.start)
+            y = self._from(y)
+            self.halo.finish(y, pending)
+        else:
+            y = self._from(self.local.hessian_apply(qdata, self._to(v)))
+            self.halo.sum_planes(y)
         return self.halo.refix(y, self.fixed2, v)
 
     def hessian_diagonal(self, qdata):

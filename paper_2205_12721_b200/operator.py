@@ -445,6 +445,73 @@ class TmopProblem:
         self._count("apply")
         return self._out(y, host, out)
 
+    def hessian_apply_boundary_first(self, qdata: HessQData, v, on_planes):
+        """Hessian action of a z-slab for the multi-GPU path:
+        the first and last element layers and the two outer node planes are
+        computed first, then `on_planes(y)` is called (the caller starts the
+        halo exchange of those planes, which then overlaps the rest), then
+        the interior elements and nodes.  Returns (y, on_planes' result);
+        y is bitwise the one-shot hessian_apply.  Device tensors, box
+        lattices without the limiting term; otherwise the one-shot apply."""
+        torch = _torch()
+        m = self.mesh
+        if not (self.lattice and _is_torch(v) and v.is_cuda and self._lim is None and m.dim == 3):
+            y = self.hessian_apply(qdata, v)
+            return y, on_planes(y)
+        nx, ny, _ = m.element_counts
+        p = m.order
+        layer, ne, nn = nx * ny, m.n_elements, m.n_nodes
+        plane = (nx * p + 1) * (ny * p + 1)
+        vt, _ = self._in(v)
+        y = torch.empty_like(vt)
+        self._sync_stream()
+        a1 = min(ne, -(-layer // 16) * 16)              # range starts stay multiples of 16
+        b0 = max(a1, (ne - layer) // 16 * 16)
+        ctx, qp, vp = self._ctx, _lib.ptr(qdata.data), _lib.ptr(vt)
+        self.last_launches = 0
+
+        def elems(e0, e1):
+            if e1 > e0:
+                _lib.check(self.lib.tmop_hessian_apply_elements_range(ctx, qp, vp, e0, e1),
+                           "tmop_hessian_apply_elements_range")
+                self.last_launches += 1
+
+        def nodes(n0, n1):
+            if n1 > n0:
+                _lib.check(self.lib.tmop_hessian_apply_gather_range(ctx, vp, _lib.ptr(y), n0, n1),
+                           "tmop_hessian_apply_gather_range")
+                self.last_launches += 1
+
+        elems(0, a1)
+        elems(b0, ne)
+        nodes(0, min(plane, nn))
+        nodes(max(plane, nn - plane), nn)
+        handle = on_planes(y)
+        # interior: element slabs on the caller's stream, the E->L sum of the
+        # node layers each slab completes on a second stream behind it
+        main = torch.cuda.current_stream(self.device)
+        aux = getattr(self, "_aux", None)
+        if aux is None:
+            aux = self._aux = torch.cuda.Stream(self.device)
+        ns = max(1, min(self.pipeline_slabs // 2, (b0 - a1) // max(layer, 1)))
+        zs = [a1 + ((b0 - a1) * k // ns) // layer * layer for k in range(ns)] + [b0]
+        cuts = sorted(set([a1] + [z // 16 * 16 for z in zs[1:-1] if a1 < z // 16 * 16 < b0] + [b0]))
+        done, top = plane, max(plane, nn - plane)
+        for k in range(len(cuts) - 1):
+            elems(cuts[k], cuts[k + 1])
+            fin = top if k == len(cuts) - 2 else min(top, (cuts[k + 1] // layer) * p * plane)
+            if fin > done:
+                aux.wait_stream(main)
+                with torch.cuda.stream(aux):
+                    self._sync_stream()
+                    nodes(done, fin)
+                self._sync_stream()
+                done = fin
+        main.wait_stream(aux)
+        y.record_stream(aux)
+        self._count("apply")
+        return y, handle
+
     # Host-resident Hessian action, pipelined slab by slab over z-layers of
     # the box lattice: the H2D copy of slab k+1's new node planes, the element
     # kernel + E->L of slab k and the D2H copy of the finished node planes of

@@ -13,7 +13,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-COUNTS, ORDER, NQ = (4, 3, 6), 2, 4
+COUNTS, ORDER, NQ = (4, 3, 8), 2, 4
 
 
 def _free_port():
@@ -56,7 +56,11 @@ def _worker(rank, world, port, results):
             return float(np.linalg.norm(local.cpu().numpy() - want) / np.linalg.norm(want))
 
         out = {"lattice": bool(lp.lattice)}
-        out["apply"] = err(dp.hessian_apply(lq, vl), gp.hessian_apply(gq, v))
+        ya = dp.hessian_apply(lq, vl)
+        out["apply"] = err(ya, gp.hessian_apply(gq, v))
+        dp.overlap = True                        # boundary layers first, exchange overlapping the interior
+        out["overlap_bitwise"] = bool(torch.equal(ya, dp.hessian_apply(lq, vl)))
+        dp.overlap = False
         out["grad"] = err(dp.gradient(xl), gp.gradient(x))
         out["diag"] = err(dp.hessian_diagonal(lq), gp.hessian_diagonal(gq))
         out["obj"] = abs(dp.objective(xl) - gp.objective(x)) / abs(gp.objective(x))
@@ -93,6 +97,7 @@ def test_slab_partition_with_device_operator_matches_global():
         out = results[r]
         assert out["lattice"], out
         assert out["apply"] <= 1e-13, out
+        assert out["overlap_bitwise"], out
         assert out["grad"] <= 1e-13, out
         assert out["diag"] <= 1e-13, out
         assert out["obj"] <= 1e-13, out
