@@ -137,7 +137,7 @@ __device__ __forceinline__ double metric_mu(int metric, double tau, double I1, c
     case MU55: { double t = tau - 1.0; return t * t; }
     case MU303: return I1 * rcbrt(tau * tau) * (1.0 / 3.0) - 1.0;
     case MU7: return I1 + mfro2<D>(S) - 2.0 * D;
-    case MU302: return I1 * mfro2<D>(S) / 9.0 - 1.0;
+    case MU302: return I1 * mfro2<D>(S) * (1.0 / 9.0) - 1.0;
     default: /* MU321 */ return I1 + mfro2<D>(S) - 2.0 * D;
   }
 }
@@ -259,17 +259,36 @@ __device__ __forceinline__ void hess_template(const double (&c)[4], const double
 //   mu_321 = I1 + J - 6:      P = 2T - 2M;              H g = 2g - 2 dM[g]
 //   mu_302 = I1 J / 9 - 1:    P = (2 J T - 2 I1 M)/9;
 //       H g = (2 dJ T + 2 J g - 2 dI1 M - 2 I1 dM[g]) / 9, dJ = -2 M:g, dI1 = 2 T:g
+// Symmetric products S S^T and S^T S (6 / 3 unique entries).
+template <int D>
+__device__ __forceinline__ void nt_sym(const double (&S)[D][D], double (&SSt)[D][D], double (&StS)[D][D]) {
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = i; j < D; ++j) {
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        a += S[i][k] * S[j][k];
+        b += S[k][i] * S[k][j];
+      }
+      SSt[i][j] = SSt[j][i] = a;
+      StS[i][j] = StS[j][i] = b;
+    }
+}
+
 template <int D>
 __device__ __forceinline__ void nt_first(int metric, const double (&T)[D][D], const double (&S)[D][D], double (&P)[D][D]) {
-  double SSt[D][D], M[D][D];
-  mmulT<D>(S, S, SSt);
+  double SSt[D][D], StS[D][D], M[D][D];
+  nt_sym<D>(S, SSt, StS);
   mmul<D>(SSt, S, M);
   if (metric == MU302) {
     const double I1 = mfro2<D>(T), J = mfro2<D>(S);
+    const double ct = (2.0 / 9.0) * J, cm = -(2.0 / 9.0) * I1;
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
-      for (int j = 0; j < D; ++j) P[i][j] = (2.0 * J * T[i][j] - 2.0 * I1 * M[i][j]) / 9.0;
+      for (int j = 0; j < D; ++j) P[i][j] = ct * T[i][j] + cm * M[i][j];
   } else {
 #pragma unroll
     for (int i = 0; i < D; ++i)
@@ -278,52 +297,44 @@ __device__ __forceinline__ void nt_first(int metric, const double (&T)[D][D], co
   }
 }
 
+// With dS = -S g^T S:  dM = dS S^T S + S dS^T S + S S^T dS
+//                         = -[(S g^T) M + (S S^T g)(S^T S) + (M g^T) S]
+// (S (S^T S) = (S S^T) S = M), three 3x3 products instead of seven.
 template <int D>
 __device__ __forceinline__ void nt_hess(int metric, double w, const double (&S)[D][D], const double (&T)[D][D],
                                         const double (&g)[D][D], double (&z)[D][D]) {
-  double SSt[D][D], M[D][D], dS[D][D], tmp[D][D], dM[D][D];
-  mmulT<D>(S, S, SSt);           // S S^T
-  mmul<D>(SSt, S, M);            // M = S S^T S
-  // dS = -S g^T S
-  mmulT<D>(S, g, tmp);           // S g^T
-  mmul<D>(tmp, S, dS);
-#pragma unroll
-  for (int i = 0; i < D; ++i)
-#pragma unroll
-    for (int j = 0; j < D; ++j) dS[i][j] = -dS[i][j];
-  // dM = dS (S^T S) + S dS^T S + (S S^T) dS
-  double StS[D][D];
+  double SSt[D][D], StS[D][D], M[D][D];
+  nt_sym<D>(S, SSt, StS);
+  mmul<D>(SSt, S, M);
+  double X[D][D], Y[D][D], Z[D][D];
+  mmulT<D>(S, g, X);             // S g^T
+  mmul<D>(SSt, g, Y);            // S S^T g
+  mmulT<D>(M, g, Z);             // M g^T
+  double nM[D][D];               // -dM[g]
 #pragma unroll
   for (int i = 0; i < D; ++i)
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < D; ++k) s += S[k][i] * S[k][j];
-      StS[i][j] = s;
+      for (int k = 0; k < D; ++k) s += X[i][k] * M[k][j] + Y[i][k] * StS[k][j] + Z[i][k] * S[k][j];
+      nM[i][j] = s;
     }
-  double a1[D][D], a2[D][D], a3[D][D];
-  mmul<D>(dS, StS, a1);
-  mmulT<D>(S, dS, tmp);          // S dS^T
-  mmul<D>(tmp, S, a2);
-  mmul<D>(SSt, dS, a3);
-#pragma unroll
-  for (int i = 0; i < D; ++i)
-#pragma unroll
-    for (int j = 0; j < D; ++j) dM[i][j] = a1[i][j] + a2[i][j] + a3[i][j];
   if (metric == MU302) {
     const double I1 = mfro2<D>(T), J = mfro2<D>(S);
     const double dJ = -2.0 * mdot<D>(M, g), dI1 = 2.0 * mdot<D>(T, g);
+    const double c = (2.0 / 9.0) * w;
+    const double ct = c * dJ, cg = c * J, cm = -c * dI1, cn = c * I1;
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
-      for (int j = 0; j < D; ++j)
-        z[i][j] = w * ((2.0 * dJ * T[i][j] + 2.0 * J * g[i][j] - 2.0 * dI1 * M[i][j] - 2.0 * I1 * dM[i][j]) / 9.0);
+      for (int j = 0; j < D; ++j) z[i][j] = ct * T[i][j] + cg * g[i][j] + cm * M[i][j] + cn * nM[i][j];
   } else {
+    const double c = 2.0 * w;
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
-      for (int j = 0; j < D; ++j) z[i][j] = w * (2.0 * g[i][j] - 2.0 * dM[i][j]);
+      for (int j = 0; j < D; ++j) z[i][j] = c * (g[i][j] + nM[i][j]);
   }
 }
 

@@ -73,6 +73,10 @@ struct XlPad {
                                        : (N == 4 ? Q * 5 : (Q == 3 ? 21 : Q == 4 ? 21 : Q == 6 ? 33 : Q * W_QY));
 };
 
+#ifndef TMOP_XL_NT_MINB
+#define TMOP_XL_NT_MINB 0
+#endif
+
 template <int N, int Q>
 struct XlCfg {
   static constexpr int EPB = XlPad<N, Q>::EPB;
@@ -114,6 +118,7 @@ struct XlCfg {
   template <int KIND>
   static constexpr int minb() {
     return TMOP_XL_MINB ? TMOP_XL_MINB
+           : (KIND == K_APPLY_NT && TMOP_XL_NT_MINB) ? TMOP_XL_NT_MINB
                         : cmax(1, 65536 / (WARPS * 32 *
                                            (xl_backward<KIND>() ? (N <= 2 ? 168 : N == 3 ? 248 : 255)
                                                                 : (N <= 3 ? 128 : 168))));
