@@ -216,14 +216,7 @@ __device__ __forceinline__ void xl_point(int metric, const double (&qd)[11], con
   }
 }
 
-// cp.async (LDGSTS): global -> shared without register staging.
-__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
 // TMA bulk store shared -> global (bulk_group completion) and its fences.
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_store(void *dst, const void *src, uint32_t bytes) {
@@ -235,7 +228,6 @@ __device__ __forceinline__ void bulk_store(void *dst, const void *src, uint32_t 
 }
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // x-line point work of the forward-only / gradient kinds at one point:
 // J = the Jacobian dx/dxi (operator.py:252-292 restated like the work-item
