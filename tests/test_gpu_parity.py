@@ -480,3 +480,50 @@ def test_overlapped_apply_and_minres_match_one_shot(rng, monkeypatch):
     assert torch.equal(out["1"][0], out["8"][0])
     assert out["1"][2] == out["8"][2] == 20
     assert rel(out["8"][1], out["1"][1].cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.parametrize("order", [1, 2, 3, 4])
+def test_properties_at_bench_size(order):
+    """BASELINE's full sizes (bench.ORDERS: ~1e8 DOFs, p = 2 is C3), checked
+    through size-independent properties: symmetry u.Hv = v.Hu on free dofs,
+    linearity, H v against a central difference of the gradient, constrained
+    outputs equal to v, and the overlapped (z-slab) action bitwise equal to
+    the one-shot elements + E->L path."""
+    import gc
+
+    import torch
+
+    import paper_2205_12721_b200 as P
+    from bench import ORDERS, perturbed_x
+    n, nq = ORDERS[order]
+    mesh = P.build_box(3, (n, n, n), order)
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), nq)
+    x = torch.from_numpy(perturbed_x(mesh)).cuda()
+    fixed = torch.from_numpy(mesh.fixed_mask.ravel()).cuda()
+    gen = torch.Generator(device="cuda").manual_seed(order)
+    u = torch.randn(mesh.n_dofs, dtype=torch.float64, device="cuda", generator=gen)
+    v = torch.randn(mesh.n_dofs, dtype=torch.float64, device="cuda", generator=gen)
+    qd = p.hessian_setup(x)
+    Hu, Hv = p.hessian_apply(qd, u), p.hessian_apply(qd, v)
+    assert torch.equal(Hv[fixed], v[fixed])
+    uf, vf = u * ~fixed, v * ~fixed
+    Huf, Hvf = p.hessian_apply(qd, uf), p.hessian_apply(qd, vf)
+    lhs, rhs = float(uf @ Hvf), float(vf @ Huf)
+    assert abs(lhs - rhs) <= 1e-10 * max(1.0, abs(lhs))
+    H2 = p.hessian_apply(qd, 1.7 * u - 0.4 * v)
+    assert float((H2 - (1.7 * Hu - 0.4 * Hv)).norm() / H2.norm()) <= 1e-13
+    # one-shot elements + E->L (the overlapped path's reference)
+    y1 = torch.empty_like(v)
+    p._sync_stream()
+    from paper_2205_12721_b200 import _lib
+    _lib.check(p.lib.tmop_hessian_apply_elements(p._ctx, _lib.ptr(qd.data), _lib.ptr(v)), "elements")
+    _lib.check(p.lib.tmop_hessian_apply_gather(p._ctx, _lib.ptr(v), _lib.ptr(y1)), "gather")
+    assert torch.equal(y1, Hv)
+    d = (1e-3 / (n * order)) * vf / float(vf.abs().max())     # 1e-3 of the node spacing
+    fd = (p.gradient(x + d) - p.gradient(x - d)) / 2
+    Hd = p.hessian_apply(qd, d)
+    free = ~fixed
+    assert float((Hd[free] - fd[free]).norm() / fd[free].norm()) <= 1e-5
+    del qd, Hu, Hv, Huf, Hvf, H2, y1, fd, Hd
+    gc.collect()
+    torch.cuda.empty_cache()
