@@ -527,3 +527,46 @@ def test_properties_at_bench_size(order):
     del qd, Hu, Hv, Huf, Hvf, H2, y1, fd, Hd
     gc.collect()
     torch.cuda.empty_cache()
+
+
+def test_diagonal_energy_gradient_at_c3_size():
+    """C3 (160^3, p = 2, n_q = 4): the assembled diagonal equals e_i^T H e_i
+    for sampled free dofs (one action per probe, several probes at once on
+    dofs far apart), and the gradient is the derivative of the energy."""
+    import torch
+
+    import paper_2205_12721_b200 as P
+    from bench import ORDERS, perturbed_x
+    n, nq = ORDERS[2]
+    mesh = P.build_box(3, (n, n, n), 2)
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), nq)
+    x = torch.from_numpy(perturbed_x(mesh)).cuda()
+    qd = p.hessian_setup(x)
+    dg = p.hessian_diagonal(qd)
+    fixed = mesh.fixed_mask.ravel()
+    rng = np.random.default_rng(7)
+    free = np.nonzero(~fixed)[0]
+    probes = np.sort(rng.choice(free, 64, replace=False))
+    # probes more than 2 elements apart share no element: one action gives all 64 columns' diagonals
+    NX = n * 2 + 1
+    node = probes % mesh.n_nodes
+    ix, iy, iz = node % NX, (node // NX) % NX, node // (NX * NX)
+    keep = [0]
+    for k in range(1, len(probes)):
+        if all(max(abs(ix[k] - ix[j]), abs(iy[k] - iy[j]), abs(iz[k] - iz[j])) > 4 for j in keep):
+            keep.append(k)
+    probes = probes[keep]
+    e = torch.zeros(mesh.n_dofs, dtype=torch.float64, device="cuda")
+    e[torch.from_numpy(probes).cuda()] = 1.0
+    He = p.hessian_apply(qd, e)
+    got, want = dg[torch.from_numpy(probes).cuda()], He[torch.from_numpy(probes).cuda()]
+    assert float((got - want).abs().max() / want.abs().max()) <= 1e-12
+    # energy / gradient consistency: (F(x + d) - F(x - d)) / 2 = g . d + O(|d|^3)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    d = torch.randn(mesh.n_dofs, dtype=torch.float64, device="cuda", generator=gen)
+    d = d * torch.from_numpy(~fixed).cuda() * (1e-3 / (n * 2)) / float(d.abs().max())
+    g = p.gradient(x)
+    lhs = (p.objective(x + d) - p.objective(x - d)) / 2
+    rhs = float(g @ d)
+    assert abs(lhs - rhs) <= 1e-6 * abs(rhs)
+    assert p.min_det_jacobian(x) > 0
