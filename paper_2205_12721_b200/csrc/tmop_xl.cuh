@@ -73,6 +73,9 @@ struct XlPad {
                                        : (N == 4 ? Q * 5 : (Q == 3 ? 21 : Q == 4 ? 21 : Q == 6 ? 33 : Q * W_QY));
 };
 
+#ifndef TMOP_XL_GRAD_MINB
+#define TMOP_XL_GRAD_MINB 0
+#endif
 #ifndef TMOP_XL_P1_MINB
 #define TMOP_XL_P1_MINB 3
 #endif
@@ -125,6 +128,7 @@ struct XlCfg {
            // p = 1, n_q = 3 action (144-thread CTAs): 3 CTAs / SM at a 128-register cap (small spill)
            // beat 2 CTAs at 166 registers: overlapped apply 6.46 -> 6.12 ms
            : (KIND == K_APPLY && N <= 2 && Q == 3) ? TMOP_XL_P1_MINB
+           : (KIND == K_GRAD && TMOP_XL_GRAD_MINB) ? TMOP_XL_GRAD_MINB
                         : cmax(1, 65536 / (WARPS * 32 *
                                            (xl_backward<KIND>() ? (N <= 2 ? 168 : N == 3 ? 248 : 255)
                                                                 : (N <= 3 ? 128 : 168))));
