@@ -509,6 +509,7 @@ class TmopProblem:
                 done = fin
         main.wait_stream(aux)
         y.record_stream(aux)
+        nodes(done, top)   # (no interior slab: the remaining node layers, all elements done)
         self._count("apply")
         return y, handle
 
