@@ -12,9 +12,12 @@ are far larger than L2, so no flush is needed between steps.
 Also reported: per-order throughput (p = 1..4 at ~1e8 DOFs, p = 1 at 2.4e7),
 the roofline of the dominant kernel (element kernel, HBM-bound), e2e through
 the public API with pinned host buffers, one Newton iteration (paper
-protocol: MINRES fixed at 20) and the CPU baseline (C/OpenMP oracle port of
-the reference apply, bounded sample).  `--impl reference` times only the CPU
-port on the host cores (the reference itself is Python and cannot travel).
+protocol: MINRES fixed at 20) and the CPU baseline: the reference's own
+`TmopProblem.hessian_apply` (tmopbench pip-installed into baseline/_ref,
+numba from the image) on the host cores, bounded sample, with the C/OpenMP
+oracle port beside it.  `--impl reference` times the reference alone
+(rank 0; other ranks exit without work).  `--gpus N` (N > 1) without a
+launcher starts N ranks itself (torch.distributed.run, 127.0.0.1).
 """
 
 from __future__ import annotations
@@ -353,8 +356,9 @@ def newton_iteration(prob, x):
             "alpha": ls.alpha, "initial_gradient_ms": 1e3 * t_pre}
 
 
-def cpu_baseline(order=2, n=40, budget_s=12.0):
-    """C/OpenMP oracle port of the reference apply on a bounded sample."""
+def cpu_baseline_port(order=2, n=40, budget_s=12.0, threads=0):
+    """C/OpenMP oracle port of the reference apply on a bounded sample
+    (secondary CPU number: the reference's algorithm in C, all cores)."""
     from oracle import tmop_oracle as O
     from oracle.cpu_apply import CpuApply
     nq = order + 2
@@ -363,7 +367,7 @@ def cpu_baseline(order=2, n=40, budget_s=12.0):
     x = O.perturb(om, np.random.default_rng(SEED), 0.2)
     v = np.random.default_rng(1).standard_normal(x.shape)
     qd = prob.hessian_setup(x)
-    ca = CpuApply(prob, qd)
+    ca = CpuApply(prob, qd, threads)
     ca(v)
     times = []
     t_start = time.perf_counter()
@@ -376,6 +380,97 @@ def cpu_baseline(order=2, n=40, budget_s=12.0):
             "sample": f"p={order} {n}^3 elements ({om.n_dofs} DOFs), n_q={nq}, mu_303; best of {len(times)} "
                       f"applies of the C/OpenMP oracle port (oracle/tmop_cpu.c)",
             "cpu_model": _cpu_model()}
+
+
+# ----------------------------------------------------------------------------
+# The reference itself (tmopbench, pip-installed into baseline/_ref, which
+# travels to the GPU box; numba / numpy / scipy are in the image).  Its
+# TmopProblem.hessian_apply (operator.py:401-418) is timed on the host cores:
+# NUMBA_NUM_THREADS = the cores this process may use (the reference CLI's
+# --threads does not set it, cli.py:63-65), one JIT warm-up, then the timed
+# applies.  Run in a subprocess so the thread count is fixed before numba loads.
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def ref_probe(n, order, threads, steps, warmup):
+    """Child process body: build the reference problem on an n^3 p=order
+    perturbed cube (n_q = p + 2, mu_303, ideal shape), set up the Q-data
+    and time `steps` reference applies after `warmup` untimed ones."""
+    sys.path.insert(0, REF_DIR)
+    import tmopbench as tb
+    nq = order + 2
+    t0 = time.perf_counter()
+    mesh = tb.build_box(3, (n, n, n), order)
+    prob = tb.TmopProblem(mesh, tb.ObjectiveConfig(tb.MetricId.MU_303, tb.TargetSpec(tb.TargetKind.IDEAL_UNIT)), nq)
+    x = perturbed_x(mesh)
+    v = np.random.default_rng(1).standard_normal(mesh.n_dofs)
+    qd = prob.hessian_setup(x)
+    t_setup = time.perf_counter() - t0
+    for _ in range(warmup):
+        prob.hessian_apply(qd, v)
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        y = prob.hessian_apply(qd, v)
+        times.append(time.perf_counter() - t)
+    tot = sum(times)
+    return {"n": n, "order": order, "n_quad": nq, "n_dofs": mesh.n_dofs, "threads": threads, "steps": steps,
+            "warmup": warmup, "total_s": tot, "mean_s": tot / steps, "best_s": min(times),
+            "gdofs": mesh.n_dofs * steps / tot / 1e9, "setup_and_build_s": t_setup,
+            "y_norm": float(np.linalg.norm(y))}
+
+
+def run_ref_probe(n, order, threads, steps, warmup, timeout=1800):
+    """Run ref_probe in a child with the thread count fixed (numba reads
+    NUMBA_NUM_THREADS at import)."""
+    env = dict(os.environ)
+    env.update(NUMBA_NUM_THREADS=str(threads), OMP_NUM_THREADS=str(threads), OPENBLAS_NUM_THREADS=str(threads),
+               MKL_NUM_THREADS=str(threads), PYTHONDONTWRITEBYTECODE="1")
+    env.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "tmop_bench_numba_cache"))
+    cmd = [sys.executable, os.path.abspath(__file__), "--ref-probe", f"{n},{order},{threads},{steps},{warmup}"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
+    if r.returncode != 0:
+        raise RuntimeError(f"reference probe failed: {r.stderr[-2000:]}")
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def reference_available():
+    if not os.path.isdir(os.path.join(REF_DIR, "tmopbench")):
+        return False, "baseline/_ref/tmopbench is not installed (pip install --target baseline/_ref /root/reference/pkg)"
+    try:
+        import numba  # noqa: F401
+    except Exception as err:
+        return False, f"numba unavailable: {err}"
+    return True, ""
+
+
+REF_SAMPLE_N = 76        # p=2, 76^3 hexes: 10.6 M DOFs (BASELINE.md section 3: >= 1e7 DOF)
+REF_SMALL_N = 24         # 1-thread sample: p=2, 24^3 hexes (352,947 DOFs)
+
+
+def cpu_baseline(budget_s=25.0):
+    """The reference's own TmopProblem.hessian_apply on the host cores
+    (kind "reference"), bounded sample: p=2 at 40^3 hexes (1.59 M DOFs),
+    applies for ~budget_s."""
+    ok, why = reference_available()
+    if not ok:
+        cb = cpu_baseline_port(HEADLINE_P, 40)
+        cb["note"] = f"reference unavailable ({why}); C/OpenMP port timed instead"
+        return cb
+    cores = host_cores()
+    r = run_ref_probe(40, HEADLINE_P, cores, 3, 1)
+    return {"value": r["gdofs"], "unit": "GDOF/s", "cores": cores, "kind": "reference",
+            "sample": f"reference tmopbench TmopProblem.hessian_apply (operator.py:401-418, baseline/_ref), p=2 "
+                      f"40^3 hexes ({r['n_dofs']} DOFs), n_q=4, mu_303, NUMBA_NUM_THREADS={cores}; "
+                      f"{r['steps']} timed applies after 1 warm-up",
+            "seconds_per_apply": r["mean_s"], "cpu_model": _cpu_model()}
 
 
 def _cpu_model():
@@ -492,6 +587,61 @@ def run_distributed(args, rank, world, local, device, metric, config):
         print(json.dumps(line))
 
 
+def self_launch(args):
+    """`bench.py --gpus N` (N > 1) without a launcher: start N ranks under
+    torch.distributed.run on 127.0.0.1 and pass their output through; fail
+    loudly when the box has fewer than N GPUs."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but only {have} CUDA device(s) visible"}),
+              file=sys.stderr)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def reference_arm(args, world, metric, config):
+    """`--impl reference`: the reference's own TmopProblem.hessian_apply
+    (baseline/_ref) on the host cores, rank 0 only.  One step = one
+    reference apply over a p=2, 76^3-hex perturbed cube (10.6 M DOFs,
+    BASELINE.md section 3's >= 1e7-DOF floor; CPU GDOF/s is flat in size,
+    PAPER.md:1032-1033) -- a bounded sample of the C3 workload.  Warm-up:
+    one JIT compile on a tiny mesh plus min(W, 1) untimed sample applies, so
+    the run stays within a few minutes.  A 1-thread number at 24^3 is
+    reported beside it (the reference barely scales with cores)."""
+    ok, why = reference_available()
+    if not ok:
+        print(json.dumps({"impl": "reference", "unavailable": why}))
+        return
+    cores = host_cores()
+    run_ref_probe(2, 1, cores, 1, 1)                     # numba JIT (cache dir under /tmp)
+    big = run_ref_probe(REF_SAMPLE_N, HEADLINE_P, cores, args.steps, min(args.warmup, 1), timeout=3600)
+    one = run_ref_probe(REF_SMALL_N, HEADLINE_P, 1, 2, 1)
+    sample = (f"reference tmopbench TmopProblem.hessian_apply (operator.py:401-418; pip-installed to baseline/_ref), "
+              f"p=2, {REF_SAMPLE_N}^3 hexes ({big['n_dofs']} DOFs), n_q=4, mu_303, ideal shape, same perturbed-x "
+              f"recipe and v seed as our arm; NUMBA_NUM_THREADS={cores}")
+    cb = {"value": big["gdofs"], "unit": "GDOF/s", "cores": cores, "kind": "reference", "sample": sample,
+          "cpu_model": _cpu_model(),
+          "one_thread": {"value": one["gdofs"], "unit": "GDOF/s", "cores": 1,
+                         "sample": f"p=2, {REF_SMALL_N}^3 hexes ({one['n_dofs']} DOFs), NUMBA_NUM_THREADS=1",
+                         "seconds_per_apply": one["mean_s"]}}
+    line = {"impl": "reference", "metric": metric, "value": big["gdofs"], "unit": "GDOF/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * big["mean_s"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (perturbed cube, seeded)", "config": config, "cpu_baseline": cb,
+            "e2e": {"value": big["gdofs"], "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "warmup_note": f"numba JIT on a 2^3 mesh + {min(args.warmup, 1)} untimed sample apply(s)",
+            "reference_setup_s": big["setup_and_build_s"]}
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -502,8 +652,21 @@ def main():
     ap.add_argument("--no-newton", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--force-dist", action="store_true", help="run the z-slab (NCCL) path even with one rank")
+    ap.add_argument("--ref-probe", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.ref_probe:
+        n, order, threads, steps, warmup = (int(t) for t in args.ref_probe.split(","))
+        print(json.dumps(ref_probe(n, order, threads, steps, warmup)))
+        return
+    if args.warmup < 3 and args.impl == "ours":
+        ap.error("--warmup must be >= 3")
+    launched = "RANK" in os.environ
+    if args.gpus > 1 and not launched and args.impl == "ours":
+        self_launch(args)
     rank, world, local = dist_env()
+    if launched and world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), file=sys.stderr)
+        sys.exit(2)
     n_h, nq_h = ORDERS[HEADLINE_P]
     config = {"workload": f"C3: 3D hex perturbed unit cube, p={HEADLINE_P}, {n_h}^3 elements, n_q={nq_h}, "
                           f"mu_303, ideal-shape target (amp 0.2 h/p^2, seed {SEED})",
@@ -514,13 +677,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = cpu_baseline(HEADLINE_P, 40, budget_s=max(3.0, 1.5 * args.steps))
-        line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": "GDOF/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
-                "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "GDOF/s", "h2d_bytes_per_step": 0,
-                                            "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        reference_arm(args, world, metric, config)
         return
 
     import torch
@@ -599,7 +756,8 @@ def main():
     if not args.no_newton:
         line["kershaw_paper_table"] = kershaw_paper_table()
     if world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(HEADLINE_P, 40)
+        line["cpu_baseline"] = cpu_baseline()
+        line["cpu_baseline_port"] = cpu_baseline_port(HEADLINE_P, 40)
     print(json.dumps(line))
     if world > 1:
         torch.distributed.barrier()

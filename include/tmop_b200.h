@@ -64,7 +64,9 @@ typedef struct {
  * (order+1)) row-major tables B[q][i] = l_i(chi_q), G[q][i] = l_i'(chi_q)
  * (fe.py:143-160); w1 is the HOST 1D quadrature weight vector (n_quad)
  * (fe.py:126-140).  fixed is uint8 per node, bit a set <=> component a
- * constrained (mesh.py:159-160).  l2e_offsets (n_nodes + 1, int64) and
+ * constrained (mesh.py:159-160); the allocation must be readable up to
+ * round_up(n_nodes, 4) bytes (the element kernels fetch the aligned 32-bit
+ * word holding a node's flags).  l2e_offsets (n_nodes + 1, int64) and
  * l2e_index (n_elements * (order+1)^dim, uint32 = e * Np + local) give, for
  * every node, its element-local copies in ascending element order -- the
  * summation order of np.add.at in fe.py:189-204.  stream is a
@@ -78,6 +80,12 @@ int tmop_ctx_create(tmop_ctx **out, int dim, int order, int n_quad,
                     double spatial_weight, void *stream);
 int tmop_ctx_destroy(tmop_ctx *ctx);
 int tmop_ctx_set_stream(tmop_ctx *ctx, void *stream);
+/* Slab-overlapped Hessian action on lattices (tmop_hessian_apply, MINRES
+ * steps): the element kernel runs in `slabs` z-slabs (1..30; 1 = one-shot)
+ * with the E->L of finished node planes on a second stream, for meshes of
+ * at least min_elements elements.  Defaults: 8 slabs (TMOP_APPLY_SLABS),
+ * 262144 elements (TMOP_OVERLAP_MIN).  Results are bitwise identical. */
+int tmop_ctx_set_apply_overlap(tmop_ctx *ctx, int slabs, int64_t min_elements);
 /* Change target scale (build_targets, metrics.py:333-345) after creation. */
 int tmop_ctx_set_target(tmop_ctx *ctx, double inv_scale, double det_w);
 
@@ -133,8 +141,10 @@ int tmop_hessian_apply_gather(tmop_ctx *ctx, const double *v, double *y);
 
 /* Streaming pieces of the same action for host-resident pipelines
  * (H2D of v / element kernel / E->L / D2H of y overlapped slab by slab):
- * the element kernel over elements [e_begin, e_end) (e_begin % 16 == 0;
- * reads v at those elements' nodes only), and the E->L sum + constraint
+ * the element kernel over elements [e_begin, e_end) (e_begin % 16 == 0 and
+ * e_end % 16 == 0 or e_end == n_elements, else TMOP_ERR_ARG: the kernels
+ * write whole 16-element groups of the E-vector; reads v at those elements'
+ * nodes only), and the E->L sum + constraint
  * fix-up for nodes [n_begin, n_end) (every element holding those nodes must
  * have been processed).  Results are bitwise identical to
  * tmop_hessian_apply. */

@@ -43,6 +43,7 @@ _SIGS = {
                         C.POINTER(_D), C.POINTER(_D), C.POINTER(_D), _INT, _D, _D, _D, _P],
     "tmop_ctx_destroy": [_P],
     "tmop_ctx_set_stream": [_P, _P],
+    "tmop_ctx_set_apply_overlap": [_P, _INT, _I64],
     "tmop_ctx_set_target": [_P, _D, _D],
     "tmop_ctx_set_lattice": [_P, _INT, _INT, _INT, _P],
     "tmop_hessian_apply_elements_range": [_P, _P, _P, _I64, _I64],

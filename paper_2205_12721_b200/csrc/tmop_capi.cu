@@ -66,9 +66,14 @@ struct tmop_ctx {
   cudaStream_t s2;
   cudaEvent_t ev[33];
   int ov_slabs;
+  int64_t ov_min;    // fewest elements for the overlapped path
   double *hist;      // MINRES residual history (device, optional)
   int hist_cap;
 };
+
+// Slab-overlapped paths only pay off for long applies (>= ~0.5 ms); below
+// this many elements the extra launches cost more than the hidden gather.
+static const int64_t OVERLAP_MIN_ELEMENTS = getenv("TMOP_OVERLAP_MIN") ? atoll(getenv("TMOP_OVERLAP_MIN")) : 262144;
 
 namespace tmop {
 int launch_elem(int dim, int n1, int nq, int kind, ElemArgs &a, const Tab &t, cudaStream_t s) {
@@ -235,6 +240,7 @@ int tmop_ctx_create(tmop_ctx **out, int dim, int order, int n_quad, int64_t n_el
     const char *ev = getenv("TMOP_APPLY_SLABS");
     c->ov_slabs = ev ? atoi(ev) : 8;
     if (c->ov_slabs > 30) c->ov_slabs = 30;
+    c->ov_min = OVERLAP_MIN_ELEMENTS;
   }
   cudaError_t e = cudaSuccess;
   // E-vector: element count padded to whole 16-element groups (interleaved layout)
@@ -277,6 +283,14 @@ int tmop_ctx_destroy(tmop_ctx *c) {
 int tmop_ctx_set_stream(tmop_ctx *c, void *stream) {
   if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
   c->stream = (cudaStream_t)stream;
+  return TMOP_OK;
+}
+
+int tmop_ctx_set_apply_overlap(tmop_ctx *c, int slabs, int64_t min_elements) {
+  if (!c) return fail(TMOP_ERR_ARG, "NULL context");
+  if (slabs < 1 || slabs > 30 || min_elements < 0) return fail(TMOP_ERR_ARG, "slabs must be in [1, 30], min >= 0");
+  c->ov_slabs = slabs;
+  c->ov_min = min_elements;
   return TMOP_OK;
 }
 
@@ -420,9 +434,6 @@ int tmop_hessian_setup(tmop_ctx *c, const double *x, double *qdata, tmop_det_sta
   return TMOP_OK;
 }
 
-// Slab-overlapped paths only pay off for long applies (>= ~0.5 ms); below
-// this many elements the extra launches cost more than the hidden gather.
-static const int64_t OVERLAP_MIN_ELEMENTS = getenv("TMOP_OVERLAP_MIN") ? atoll(getenv("TMOP_OVERLAP_MIN")) : 262144;
 
 // Overlapped action on a verified lattice: z-slab element launches on the
 // context stream; after each, the E->L sum of the node planes that slab
@@ -482,7 +493,7 @@ int tmop_hessian_apply(tmop_ctx *c, const double *qdata, const double *v, double
   if (!c || !qdata || !v || !y) return fail(TMOP_ERR_ARG, "NULL argument");
   // (p <= 3: the x-line element kernel leaves register room for the gather's
   // CTAs; measured 4-5 % faster there, slower at p = 4)
-  if (c->lat_p > 0 && c->n1 <= 4 && !c->lim_on && c->ov_slabs > 1 && c->ne >= OVERLAP_MIN_ELEMENTS)
+  if (c->lat_p > 0 && c->n1 <= 4 && !c->lim_on && c->ov_slabs > 1 && c->ne >= c->ov_min)
     return apply_overlapped(c, qdata, v, y);
   int rc = tmop_hessian_apply_elements(c, qdata, v);
   if (rc) return rc;
@@ -504,8 +515,12 @@ int tmop_hessian_apply_elements_range(tmop_ctx *c, const double *qdata, const do
                                       int64_t e_end) {
   if (!c || !qdata || !v) return fail(TMOP_ERR_ARG, "NULL argument");
   if (c->lim_on) return fail(TMOP_ERR_ARG, "range apply does not support the limiting term");
-  if (e_begin < 0 || e_end > c->ne || e_begin > e_end || (e_begin & 15))
-    return fail(TMOP_ERR_ARG, "element range [%lld, %lld) invalid (begin must be a multiple of 16, end <= %lld)",
+  // both ends on a 16-element group boundary (or end == n_elements): the
+  // element kernels write whole groups of the E-vector, so a range ending
+  // inside a group would overwrite E entries belonging to the next range
+  if (e_begin < 0 || e_end > c->ne || e_begin > e_end || (e_begin & 15) || ((e_end & 15) && e_end != c->ne))
+    return fail(TMOP_ERR_ARG,
+                "element range [%lld, %lld) invalid (begin and end must be multiples of 16, or end == %lld)",
                 (long long)e_begin, (long long)e_end, (long long)c->ne);
   if (e_begin == e_end) return TMOP_OK;
   ElemArgs a = base_args(c);
@@ -693,7 +708,7 @@ int tmop_minres_step_op(tmop_ctx *c, const double *qdata, int64_t n, double *Av,
   if (!c || !qdata || !st2) return fail(TMOP_ERR_ARG, "NULL argument");
   if (n != c->nn * c->dim) return fail(TMOP_ERR_ARG, "vector length %lld != dim * n_nodes", (long long)n);
   tmop_minres_state *cur = st2 + (k & 1), *nxt = st2 + ((k + 1) & 1);
-  if (c->lat_p > 0 && c->n1 <= 4 && !c->lim_on && c->ov_slabs > 1 && c->ne >= OVERLAP_MIN_ELEMENTS) {
+  if (c->lat_p > 0 && c->n1 <= 4 && !c->lim_on && c->ov_slabs > 1 && c->ne >= c->ov_min) {
     // overlapped: element kernel by z-slab on the context stream, the fused
     // E->L + K1 of each finished node range on the second stream (its K1
     // partials in a per-slab block of vpart1), then K2 / K3 reduce them all

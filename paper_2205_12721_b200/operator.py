@@ -81,9 +81,11 @@ class DeviceMesh:
         self.n_elements = mesh.n_elements
         restr = torch.from_numpy(np.ascontiguousarray(mesh.restriction, dtype=np.int32)).to(device)
         self.restriction = restr
-        flags = np.zeros(mesh.n_nodes, dtype=np.uint8)
+        # padded to a multiple of 4 bytes: the element kernels fetch the
+        # aligned 32-bit word holding fixed[node] (tmop_b200.h, ctx_create)
+        flags = np.zeros((mesh.n_nodes + 3) // 4 * 4, dtype=np.uint8)
         for a in range(mesh.dim):
-            flags |= (mesh.fixed_mask[a].astype(np.uint8) << a)
+            flags[:mesh.n_nodes] |= (mesh.fixed_mask[a].astype(np.uint8) << a)
         self.fixed = torch.from_numpy(flags).to(device)
         self.fixed_mask = torch.from_numpy(np.ascontiguousarray(mesh.fixed_mask.ravel())).to(device)
         flat = restr.reshape(-1).to(torch.int64)
@@ -560,9 +562,11 @@ class TmopProblem:
             w[1] = w[-2] = 0.5
         cum = np.concatenate([[0.0], np.cumsum(w)]) / sum(w)
         zs = sorted(set(int(round(c * nz)) for c in cum[:-1]))
+        # several ramp points can round to the same z layer (nz < ~4 ns): the
+        # set() above drops them, so walk the bounds actually produced
         bounds = [z * layer // 16 * 16 for z in zs] + [ne]
         copied, done = 0, 0
-        for k in range(ns):
+        for k in range(len(bounds) - 1):
             e0, e1 = bounds[k], bounds[k + 1]
             if e1 <= e0:
                 continue
@@ -628,6 +632,12 @@ class TmopProblem:
         y = _torch().empty_like(vt)
         _lib.check(self.lib.tmop_limiting_apply(self._ctx, _lib.ptr(vt), _lib.ptr(y)), "tmop_limiting_apply")
         return self._out(y, host)
+
+    def set_apply_overlap(self, slabs: int, min_elements: int = 0) -> None:
+        """Slab-overlapped action on lattices (tmop_ctx_set_apply_overlap):
+        `slabs` z-slabs (1 = one-shot) for meshes of >= min_elements."""
+        _lib.check(self.lib.tmop_ctx_set_apply_overlap(self._ctx, int(slabs), int(min_elements)),
+                   "tmop_ctx_set_apply_overlap")
 
     # ---------------------------------------------------------- raw C-ABI
     @property

@@ -354,7 +354,11 @@ def test_lattice_rejects_non_lattice_restriction(rng):
     assert not p.lattice
 
 
-@pytest.mark.parametrize("order,nq,counts,slabs", [(2, 4, (6, 5, 9), 4), (1, 3, (7, 3, 5), 8), (3, 5, (3, 4, 5), 3)])
+@pytest.mark.parametrize("order,nq,counts,slabs", [(2, 4, (6, 5, 9), 4), (1, 3, (7, 3, 5), 8), (3, 5, (3, 4, 5), 3),
+                                                    # default slab count with the ramp on and nz in 8..24:
+                                                    # several ramp points round to one z layer
+                                                    (1, 3, (4, 4, 8), 16), (2, 4, (5, 4, 12), 16),
+                                                    (1, 3, (6, 6, 24), 16), (2, 4, (3, 3, 17), 16)])
 def test_pipelined_host_apply_is_bitwise_equal(order, nq, counts, slabs, rng, monkeypatch):
     """Pinned host input: the slab-pipelined H2D / element kernel / E->L / D2H
     path returns exactly the one-shot device result."""
@@ -570,3 +574,36 @@ def test_diagonal_energy_gradient_at_c3_size():
     rhs = float(g @ d)
     assert abs(lhs - rhs) <= 1e-6 * abs(rhs)
     assert p.min_det_jacobian(x) > 0
+
+
+# C3-shaped sub-boxes: the bench grid's full x/y extent (160^2 at p = 2,
+# 107^2 at p = 3, 80^2 at p = 4) with a few z layers, so the x-line element
+# groups, the 16-element range alignment (107^2 = 11449 elements per layer is
+# not a multiple of 16) and the slab-overlapped apply run exactly as at the
+# bench size; the oracle still finishes in seconds.
+@pytest.mark.parametrize("order,nq,counts", [(2, 4, (160, 160, 3)), (3, 5, (107, 107, 3)), (4, 6, (80, 80, 2)),
+                                             (1, 3, (200, 200, 2))])
+def test_bench_shape_sub_box_matches_oracle(order, nq, counts, rng):
+    import torch
+
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(3, counts, order)
+    om = O.box_mesh(3, counts, order)
+    op = O.OracleProblem(om, O.MU_303, nq)
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), nq)
+    x = O.perturb(om, rng, 0.2)
+    v = rng.standard_normal(x.shape)
+    xd, vd = torch.from_numpy(x).cuda(), torch.from_numpy(v).cuda()
+    qd = p.hessian_setup(xd)
+    oqd = op.hessian_setup(x)
+    want = op.hessian_apply(oqd, v)
+    p.set_apply_overlap(1, 0)                      # one-shot element kernel + E->L
+    one = p.hessian_apply(qd, vd)
+    assert rel(one, want) <= TOL
+    p.set_apply_overlap(counts[2], 0)              # slab-overlapped (bench default path), one slab per layer
+    ov = p.hessian_apply(qd, vd)
+    assert torch.equal(ov, one)
+    p.set_apply_overlap(8, 262144)
+    assert rel(p.gradient(xd), op.gradient(x)) <= TOL
+    assert rel(p.hessian_diagonal(qd), op.hessian_diagonal(oqd)) <= TOL
+    assert p.objective(xd) == pytest.approx(op.objective(x), rel=TOL)

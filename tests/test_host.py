@@ -65,6 +65,8 @@ def test_l2e_map_reproduces_add_at_order():
         got[node] = acc
     assert np.array_equal(got, want)                   # same order => bitwise equal
     flags = dm.fixed.numpy()
+    assert flags.size % 4 == 0 and not flags[mesh.n_nodes:].any()   # padded to whole 32-bit words
+    flags = flags[:mesh.n_nodes]
     for a in range(3):
         assert np.array_equal(((flags >> a) & 1).astype(bool), mesh.fixed_mask[a])
 

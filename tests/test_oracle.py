@@ -208,3 +208,18 @@ def test_limiting_nodal_delta_matches_reference(name):
     assert p.limiting_value(x) == pytest.approx(float(g["lim_value"]), rel=1e-12)
     assert rel(p._lim_grad2(p._x2(x)).ravel(), g["lim_gradient"]) <= 1e-12
     assert rel(p._lim_hess2(p._x2(v)).ravel(), g["lim_apply"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", [n for n in OPS if n.startswith("op3d") and "lim" not in n])
+@pytest.mark.parametrize("threads", [1, 3])
+def test_cpu_port_matches_reference(name, threads):
+    """oracle/tmop_cpu.c (the C/OpenMP restatement timed as a secondary CPU
+    baseline by bench.py) against the reference's own apply, bitwise
+    independent of the thread count."""
+    from oracle.cpu_apply import CpuApply
+    g = load_golden(name)
+    p = problem_from(g)
+    qd = p.hessian_setup(g["x"])
+    y = CpuApply(p, qd, threads)(g["v"])
+    assert rel(y, g["apply"]) <= 1e-12
+    assert np.array_equal(y, CpuApply(p, qd, 2)(g["v"]))
