@@ -324,6 +324,35 @@ def c1_solve():
     return out
 
 
+def c5_solve(n=96, max_newton=25):
+    """BASELINE configs[4] (C5) on one GPU: 3D Q2 hexes, shape+size metric
+    mu_321 with size-adaptive targets (TargetKind.SIZE_FIELD: nodal target
+    volume 'shell' field, W_q = v_q^(1/3) I), perturbed start, full Newton
+    + Jacobi-MINRES (cap 50, rtol 1e-8) to rtol 1e-10 or `max_newton`
+    iterations.  Reports the solve time, iteration counts, F and how far
+    the element volumes moved toward their targets."""
+    import torch
+
+    import paper_2205_12721_b200 as P
+    mesh = P.build_box(3, (n, n, n), 2)
+    eta = P.size_field(mesh, "shell")
+    prob = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_321, P.TargetSpec(P.TargetKind.SIZE_FIELD, size=eta)),
+                         4)
+    x0 = torch.from_numpy(perturbed_x(mesh)).cuda()
+    f0 = prob.objective(x0)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    res = P.newton_solve(x0, prob, P.NewtonConfig(max_iterations=max_newton), P.MinresConfig())
+    torch.cuda.synchronize()
+    ts = time.perf_counter() - t
+    return {"workload": f"C5 (1 GPU): 3D Q2 {n}^3 hexes, mu_321, size-field targets (shell), n_q=4, "
+                        f"full Newton + Jacobi-MINRES", "n_dofs": mesh.n_dofs, "solve_s": ts,
+            "newton_iterations": res.trace.newton_iterations, "minres_iterations": res.trace.minres_total,
+            "status": "ok" if res.success else "stopped", "message": res.message, "f_initial": f0,
+            "f_final": prob.objective(res.x), "rel_grad": res.rel_grad,
+            "ms_per_newton_iteration": 1e3 * ts / max(1, res.trace.newton_iterations)}
+
+
 def newton_iteration(prob, x):
     """One Newton iteration, paper protocol (MINRES fixed at 20 iterations,
     PAPER.md:1002-1004): setup + diagonal + MINRES + line search."""
@@ -490,101 +519,226 @@ def dist_env():
     return rank, world, local
 
 
-def run_distributed(args, rank, world, local, device, metric, config):
-    """N > 1: weak scaling over z-slabs.  The global mesh is
-    160 x 160 x (160 N) p=2 hexes; rank r owns the slab of layers
-    [160 r, 160 (r+1)) and one step = local Hessian action + NCCL sum of the
-    shared node planes with the z-neighbours (+ constraint re-fix).  Time is
-    the max over ranks; halo time is reported separately."""
+def _hash_unit(idx, salt):
+    """Counter-based uniform(-1, 1) from global indices (splitmix64): every
+    rank draws the same value for a shared node, whatever the partition."""
+    z = (idx.astype(np.uint64) + np.uint64(salt) * np.uint64(0x9E3779B97F4A7C15)) * np.uint64(0xBF58476D1CE4E5B9)
+    z ^= z >> np.uint64(31)
+    z *= np.uint64(0x94D049BB133111EB)
+    z ^= z >> np.uint64(29)
+    return (z >> np.uint64(11)).astype(np.float64) * (2.0 / 2 ** 53) - 1.0
+
+
+def slab_inputs(part, mesh, seed=SEED):
+    """x (perturbed lattice, amp 0.2 h/p^2 on free components) and v (unit
+    variance) as functions of GLOBAL (component, node) ids, so the copies of
+    a shared node plane on two ranks are identical."""
+    nx, ny, nz = part.counts
+    n_glob = (nx * part.order + 1) * (ny * part.order + 1) * (nz * part.order + 1)
+    gid = (np.arange(3, dtype=np.int64)[:, None] * n_glob
+           + np.arange(part.node_lo, part.node_hi, dtype=np.int64)[None, :]).ravel()
+    gap = (1.0 / max(part.counts)) / part.order ** 2
+    j = 0.2 * gap * _hash_unit(gid, seed)
+    j[mesh.fixed_mask.ravel()] = 0.0
+    x = mesh.coords.ravel() + j
+    v = np.sqrt(3.0) * _hash_unit(gid, seed + 1)
+    return x, v
+
+
+def dist_leg(rank, world, device, counts, order, nq, steps, warmup, group=None, sampler=None):
+    """One distributed Hessian-action leg over z-slabs: the
+    local action (slab-overlapped element kernel + E->L) then the halo plane
+    sum + constraint re-fix (library pack / NCCL send-recv / unpack), timed
+    with CUDA events per step; returns the max-over-ranks times."""
     import torch
     import torch.distributed as dist
 
     import paper_2205_12721_b200 as P
-    from paper_2205_12721_b200.distributed import DistributedProblem, SlabPartition
-    n, nq = ORDERS[HEADLINE_P]
-    counts = (n, n, n * world)
-    part = SlabPartition(counts, HEADLINE_P, world, rank)
+    from paper_2205_12721_b200.distributed import DistributedProblem, SlabPartition, allreduce_
+    part = SlabPartition(counts, order, world, rank)
     mesh = part.local_mesh_direct()
     prob = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), nq,
                          device=device)
-    dp = DistributedProblem(prob, part, mesh.fixed_mask).to(device)
-    x = torch.from_numpy(perturbed_x(mesh, seed=SEED + rank)).to(device)
-    v = torch.from_numpy(np.random.default_rng(1 + rank).standard_normal(mesh.n_dofs)).to(device)
+    dp = DistributedProblem(prob, part, mesh.fixed_mask, group=group).to(device)
+    xh, vh_np = slab_inputs(part, mesh)
+    x = torch.from_numpy(xh).to(device)
+    v = torch.from_numpy(vh_np).to(device)
     qd = prob.hessian_setup(x)
+    y = torch.empty_like(v)
     s = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        dp.hessian_apply(qd, v)
-    # timed steps: the distributed action as DistributedProblem.hessian_apply
-    # runs it by default -- the local (slab-overlapped) action, then the NCCL
-    # plane sum and re-fix, split by events so the halo time is reported
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    dist.barrier()
+    for _ in range(warmup):
+        dp.hessian_apply_into(qd, v, y)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    dist.barrier(group)
     torch.cuda.synchronize()
-    with ClockSampler(local) as cs:
-        for k in range(args.steps):
+    ctx_s = sampler if sampler is not None else _NullCtx()
+    with ctx_s:
+        for k in range(steps):
             ev[k][0].record(s)
-            y = prob.hessian_apply(qd, v)
+            prob.hessian_apply(qd, v, out=y)
             ev[k][1].record(s)
-            dp.halo.sum_planes(y)
-            dp.halo.refix(y, dp.fixed2, v)
+            dp.halo.sum_planes_device(y, 1, vfix=v)
             ev[k][2].record(s)
         torch.cuda.synchronize()
-    dist.barrier()
+    dist.barrier(group)
     total = ev[0][0].elapsed_time(ev[-1][2]) / 1e3
     halo = statistics.mean(e[1].elapsed_time(e[2]) for e in ev) / 1e3
-    # the boundary-first variant (DistributedProblem.overlap = True: outer
-    # layers + planes first, exchange overlapping the interior), for comparison
-    dp.overlap = True
-    dp.hessian_apply(qd, v)
-    b0e, b1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dist.barrier()
-    b0e.record(s)
-    for _ in range(args.steps):
-        dp.hessian_apply(qd, v)
-    b1e.record(s)
-    torch.cuda.synchronize()
-    dp.overlap = False
-    bf = b0e.elapsed_time(b1e) / 1e3
-    t = torch.tensor([total, halo, bf], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total, halo, bf = float(t[0]), float(t[1]), float(t[2])
-    global_dofs = 3 * (n * HEADLINE_P + 1) ** 2 * (n * world * HEADLINE_P + 1)
-    value = global_dofs * args.steps / total / 1e9
-    # e2e through the distributed API with pinned host buffers
-    vh = v.cpu().pin_memory()
-    yh = torch.empty_like(vh).pin_memory()
-    dist.barrier()
+    loc = statistics.mean(e[0].elapsed_time(e[1]) for e in ev) / 1e3
+    t = torch.tensor([total, halo, loc], dtype=torch.float64, device=device)
+    allreduce_(t, op=dist.ReduceOp.MAX, group=group)
+    total, halo, loc = (float(u) for u in t.cpu())
+    nx, ny, nz = counts
+    global_dofs = 3 * (nx * order + 1) * (ny * order + 1) * (nz * order + 1)
+    # e2e through the distributed public API: pinned host v -> device ->
+    # DistributedProblem.hessian_apply -> pinned host y, every step
+    vpin = v.cpu().pin_memory()
+    ypin = torch.empty_like(vpin).pin_memory()
+    dist.barrier(group)
     torch.cuda.synchronize()
     te0 = time.perf_counter()
-    for _ in range(args.steps):
-        vd = vh.to(device, non_blocking=True)
+    for _ in range(steps):
+        vd = vpin.to(device, non_blocking=True)
         yd = dp.hessian_apply(qd, vd)
-        yh.copy_(yd, non_blocking=True)
+        ypin.copy_(yd, non_blocking=True)
         torch.cuda.synchronize()
     te = torch.tensor([time.perf_counter() - te0], dtype=torch.float64, device=device)
-    dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    te = float(te.item()) / args.steps
-    if rank == 0:
-        cfg = dict(config)
-        cfg.update(workload=f"C4-style weak scaling: global {n}x{n}x{n * world} p={HEADLINE_P} hexes, n_q={nq}, "
-                            f"mu_303, z-slab per GPU", parallelism=f"z-slabs x{world} (NCCL halo plane sums)")
-        line = {"metric": metric, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (perturbed slabs, seeded)",
-                "config": cfg, "halo_ms_per_step": 1e3 * halo,
-                "halo_note": "plane exchange + re-fix after the local action, inside the timed steps",
-                "ms_per_step_boundary_first": 1e3 * bf / args.steps,
-                "halo_bytes_per_neighbor": dp.halo.bytes_per_exchange,
-                "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peaks()[0],
-                             "achieved": apply_bytes(3, HEADLINE_P, nq, mesh.n_elements, mesh.n_dofs)
-                             / (total / args.steps - halo) / 1e9,
-                             "frac": apply_bytes(3, HEADLINE_P, nq, mesh.n_elements, mesh.n_dofs)
-                             / (total / args.steps - halo) / 1e9 / peaks()[0],
-                             "traffic": None, "kernel": "local Hessian action (element kernel + E->L), per GPU"},
-                "e2e": {"value": global_dofs / te / 1e9, "unit": "GDOF/s",
-                        "h2d_bytes_per_step": 8 * mesh.n_dofs * world, "d2h_bytes_per_step": 8 * mesh.n_dofs * world},
-                "gpu_launches": 2 * OVERLAP_SLABS * args.steps, "clocks": cs.summary()}
-        print(json.dumps(line))
+    allreduce_(te, op=dist.ReduceOp.MAX, group=group)
+    te = float(te.cpu()[0]) / steps
+    out = {"counts": list(counts), "order": order, "n_quad": nq, "global_dofs": global_dofs,
+           "local_dofs": mesh.n_dofs, "local_elements": mesh.n_elements, "ms_per_step": 1e3 * total / steps,
+           "local_action_ms": 1e3 * loc, "halo_ms_per_step": 1e3 * halo,
+           "halo_bytes_per_neighbor": dp.halo.bytes_per_exchange,
+           "gdofs": global_dofs * steps / total / 1e9, "e2e_gdofs": global_dofs / te / 1e9,
+           "e2e_ms_per_step": 1e3 * te, "h2d_bytes_per_step": 8 * mesh.n_dofs * world,
+           "d2h_bytes_per_step": 8 * mesh.n_dofs * world,
+           "elem_bytes_per_rank": element_kernel_bytes(3, order, nq, mesh.n_elements, mesh.n_dofs)}
+    return out, (prob, dp, qd, x)
+
+
+class _NullCtx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+    def summary(self):
+        return None
+
+
+def dist_newton_iteration(dp, prob, x, group=None):
+    """One distributed Newton iteration, paper protocol (MINRES fixed at 20,
+    PAPER.md:1002-1004): setup + diagonal + device-resident MINRES (halo
+    sums and in-stream all-reduces) + line search; wall time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_12721_b200.distributed import allreduce_, dist_minres_device
+    torch.cuda.synchronize()
+    dist.barrier(group)
+    t0 = time.perf_counter()
+    g = dp.gradient(x)
+    f = dp.objective(x)
+    ng = float(np.sqrt(dp.dot(g, g)))
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    qd = dp.hessian_setup(x)
+    d = dp.hessian_diagonal(qd)
+    inv = 1.0 / d.abs().clamp_min(1e-12)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    dx, its, rr, _ = dist_minres_device(dp, qd, g, 20, 1e-300, inv)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    alpha = 1.0
+    for _ in range(31):
+        xt = x - alpha * dx
+        if dp.min_det_jacobian(xt) > 0.0 and dp.objective(xt) < 1.2 * f:
+            gt = dp.gradient(xt)
+            if float(np.sqrt(dp.dot(gt, gt))) < 1.2 * ng:
+                break
+        alpha *= 0.5
+    torch.cuda.synchronize()
+    t4 = time.perf_counter()
+    t = torch.tensor([t4 - t1, t2 - t1, t3 - t2, t4 - t3, t1 - t0], dtype=torch.float64, device=x.device)
+    allreduce_(t, op=dist.ReduceOp.MAX, group=group)
+    t = [1e3 * float(u) for u in t.cpu()]
+    return {"ms": t[0], "setup_diag_ms": t[1], "minres_ms": t[2], "minres_iterations": its, "line_search_ms": t[3],
+            "alpha": alpha, "initial_gradient_ms": t[4]}
+
+
+def nccl_summary():
+    """Communicator lines NCCL_DEBUG=INFO wrote to NCCL_DEBUG_FILE (set in
+    main() before the process group starts)."""
+    path = os.environ.get("NCCL_DEBUG_FILE", "")
+    if "%" in path or not path or not os.path.exists(path):
+        import glob
+        cands = sorted(glob.glob(os.path.join("/tmp", f"tmop_nccl.{os.getpid()}.log")))
+        path = cands[0] if cands else ""
+    lines = []
+    try:
+        for ln in open(path):
+            if any(k in ln for k in ("comm 0x", "NVLS", "Channel 00", "Connected all", "Using network", "P2P/")):
+                lines.append(ln.strip()[-160:])
+    except Exception:
+        pass
+    return lines[:24]
+
+
+DIST_ORDERS = {"c3_weak": (2, 160, 4), "c4": (3, 112, 5)}   # leg -> (p, elements per axis per slab, n_q)
+
+
+def run_distributed(args, rank, world, local, device, metric, config, group=None):
+    """z-slab multi-GPU legs (BASELINE configs[3]):
+      headline  C3 weak scaling: global 160 x 160 x (160 N) p=2 hexes, n_q=4,
+                one 160-layer slab per GPU (the N=1 headline's per-GPU work);
+      c4_strong Q3 (n_q=5) 112^3 total, 112/N layers per GPU;
+      c4_weak   Q3 112 x 112 x (112 N), 112 layers per GPU;
+      newton    one distributed Newton iteration on the headline mesh
+                (MINRES fixed at 20, device resident).
+    Times are CUDA events on the launching stream, max over ranks; the halo
+    (pack + NCCL send/recv + unpack/re-fix) is reported per step."""
+    p2, n2, q2 = DIST_ORDERS["c3_weak"]
+    p3, n3, q3 = DIST_ORDERS["c4"]
+    if args.dist_n:
+        n2 = n3 = args.dist_n
+    with ClockSampler(local) as cs:
+        head, (prob, dp, qd, x) = dist_leg(rank, world, device, (n2, n2, n2 * world), p2, q2, args.steps,
+                                           args.warmup, group)
+    newton = None if args.no_newton else dist_newton_iteration(dp, prob, x, group)
+    del prob, dp, qd, x
+    import gc
+    gc.collect()
+    import torch
+    torch.cuda.empty_cache()
+    strong, _ = dist_leg(rank, world, device, (n3, n3, n3), p3, q3, args.steps, args.warmup, group)
+    gc.collect()
+    torch.cuda.empty_cache()
+    weak, _ = dist_leg(rank, world, device, (n3, n3, n3 * world), p3, q3, args.steps, args.warmup, group)
+    if rank != 0:
+        return
+    peak = peaks()[0]
+    t_loc = head["local_action_ms"] / 1e3
+    achieved = head["elem_bytes_per_rank"] / t_loc / 1e9
+    cfg = dict(config)
+    cfg.update(workload=f"C3 weak scaling over z-slabs: global {n2}x{n2}x{n2 * world} p={p2} hexes, n_q={q2}, mu_303, "
+                        f"one {n2}-layer slab per GPU",
+               elements_per_axis=n2, parallelism=f"z-slabs x{world} (NCCL halo plane sums)",
+               backend=args.dist_backend)
+    line = {"metric": metric, "value": head["gdofs"], "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (perturbed slabs; inputs hashed from global ids)",
+            "config": cfg, "halo_ms_per_step": head["halo_ms_per_step"],
+            "halo_bytes_per_neighbor": head["halo_bytes_per_neighbor"],
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "kernel": "local Hessian action per GPU (element kernel + E->L, overlapped)",
+                         "algorithmic_bytes_per_launch": head["elem_bytes_per_rank"]},
+            "e2e": {"value": head["e2e_gdofs"], "unit": "GDOF/s", "h2d_bytes_per_step": head["h2d_bytes_per_step"],
+                    "d2h_bytes_per_step": head["d2h_bytes_per_step"], "ms_per_step": head["e2e_ms_per_step"]},
+            "gpu_launches": (2 * OVERLAP_SLABS + 2) * args.steps, "clocks": cs.summary(),
+            "headline_leg": head, "c4_strong": strong, "c4_weak": weak, "newton_iteration": newton,
+            "nccl": nccl_summary()}
+    print(json.dumps(line))
 
 
 def self_launch(args):
@@ -595,7 +749,7 @@ def self_launch(args):
 
     import torch
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and args.dist_backend != "gloo":   # (gloo runs share cuda:0)
         print(json.dumps({"error": f"--gpus {args.gpus} requested but only {have} CUDA device(s) visible"}),
               file=sys.stderr)
         sys.exit(2)
@@ -653,6 +807,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--force-dist", action="store_true", help="run the z-slab (NCCL) path even with one rank")
     ap.add_argument("--ref-probe", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="gloo: all ranks share cuda:0 (schema / correctness runs on a 1-GPU box)")
+    ap.add_argument("--dist-n", type=int, default=0, help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.ref_probe:
         n, order, threads, steps, warmup = (int(t) for t in args.ref_probe.split(","))
@@ -684,8 +841,26 @@ def main():
     dist_path = world > 1 or args.force_dist
     if dist_path:
         import torch.distributed as dist
+        if args.dist_backend == "gloo":
+            local = 0                       # every rank on cuda:0 (schema / correctness runs)
+        elif local >= torch.cuda.device_count():
+            print(json.dumps({"error": f"rank {rank}: LOCAL_RANK {local} but only {torch.cuda.device_count()} "
+                                       f"CUDA device(s)"}), file=sys.stderr)
+            sys.exit(2)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if "RANK" not in os.environ:            # --force-dist without a launcher: a 1-rank group
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=str(port))
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/tmop_nccl.{os.getpid()}.log")
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     device = torch.device("cuda", local if dist_path else torch.cuda.current_device())
     torch.cuda.set_device(device)
     if dist_path:
@@ -753,6 +928,10 @@ def main():
     torch.cuda.empty_cache()   # the small-problem sections below run after the 1e8-DOF ones
     line["c2_small"] = small_config_c2()
     line["c1_solve"] = c1_solve()
+    if not args.no_newton:
+        gc.collect()
+        torch.cuda.empty_cache()
+        line["c5_solve"] = c5_solve()
     if not args.no_newton:
         line["kershaw_paper_table"] = kershaw_paper_table()
     if world == 1 and not args.no_cpu:

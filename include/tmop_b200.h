@@ -88,6 +88,19 @@ int tmop_ctx_set_stream(tmop_ctx *ctx, void *stream);
 int tmop_ctx_set_apply_overlap(tmop_ctx *ctx, int slabs, int64_t min_elements);
 /* Change target scale (build_targets, metrics.py:333-345) after creation. */
 int tmop_ctx_set_target(tmop_ctx *ctx, double inv_scale, double det_w);
+/* Size-field targets (EXTENSION: the reference has constant isotropic W
+ * only, metrics.py:282-345; SPEC.md:9 lists space-dependent W as a
+ * non-goal).  volume_nodal (DEVICE, n_nodes) is a target element volume per
+ * node, interpolated to the quadrature points with B (fe.py:227-239):
+ * v_q = sum_i eta_i phi_i(chi_q), W_q = v_q^(1/d) I, so T = A / v_q^(1/d) and
+ * det W_q = v_q enter the energy / gradient / Hessian setup point by point
+ * (the Hessian action and diagonal read them from the Q-data record).  The
+ * field is material (fixed per quadrature point while x moves).  The
+ * per-point 1/s_q array is computed here, on the context stream; a v_q <= 0
+ * yields NaN (tmop_ctx_point_scale exposes the array for checks).  NULL
+ * clears it (constant W = I); tmop_ctx_set_target also clears it. */
+int tmop_ctx_set_size_field(tmop_ctx *ctx, const double *volume_nodal);
+const double *tmop_ctx_point_scale(const tmop_ctx *ctx);
 
 /* Declare that the mesh is the (nx, ny, nz) box lattice of build_box
  * (mesh.py:118-164).  The restriction is verified on the device; when it
@@ -243,6 +256,45 @@ int tmop_minres_step_op(tmop_ctx *ctx, const double *qdata, int64_t n,
                         const double *w, double *w1buf, const double *w2,
                         double *x, double rtol, tmop_minres_state *st2,
                         int k);
+
+/* ---- slab-partitioned (multi-GPU) MINRES and halo planes -------------
+ * The paper's MPI assembly P^T -- absent from the
+ * reference -- for a z-slab partition of a box lattice: local
+ * vectors are component-major (3, nn) with the shared node planes (nodes
+ * [0, plane) and [nn - plane, nn)) duplicated on both neighbours.
+ *
+ * MINRES phases (solvers.py:93-180) with every inner product taken over
+ * OWNED entries (node < n_owned in each component; nn = 0: all owned) and
+ * reduced in a fixed order into the device scalar scal[k]; between phases
+ * the caller all-reduces scal[k] (SUM) across ranks on the context stream
+ * (NCCL), so no phase needs a host round trip:
+ *   init_a: r1 = r2 = b; z = inv .* b; x = w = w2 = 0; scal[0] = b.z
+ *   init_b: beta1 = sqrt(scal[0]); v = z / beta1; state slot 0
+ *   k1:     Av -= (beta/oldb) r1 (itn >= 1); scal[0] = v.Av
+ *   k2:     alfa = scal[0]; Av -= (alfa/beta) r2; z = inv .* Av; scal[1] = Av.z
+ *   k3:     beta2 = scal[1]; Givens recurrence; w1buf, x, v updates
+ * Same buffer rotation and state-slot contract as tmop_minres_step; Av must
+ * hold the halo-summed, constraint-fixed action on entry to k1. */
+int tmop_minres_dist_init_a(tmop_ctx *ctx, int64_t n, int64_t nn, int64_t n_owned, const double *b, const double *inv,
+                            double *x, double *r1, double *r2, double *z, double *w, double *w2, double *scal);
+int tmop_minres_dist_init_b(tmop_ctx *ctx, int64_t n, const double *z, double *v, const double *scal,
+                            tmop_minres_state *st2);
+int tmop_minres_dist_k1(tmop_ctx *ctx, int64_t n, int64_t nn, int64_t n_owned, double *Av, const double *r1,
+                        const double *v, tmop_minres_state *st2, int k, double *scal);
+int tmop_minres_dist_k2(tmop_ctx *ctx, int64_t n, int64_t nn, int64_t n_owned, double *Av, const double *r2,
+                        const double *inv, double *z, tmop_minres_state *st2, int k, double *scal);
+int tmop_minres_dist_k3(tmop_ctx *ctx, int64_t n, const double *z, double *v, const double *w, double *w1buf,
+                        const double *w2, double *x, double rtol, tmop_minres_state *st2, int k, const double *scal);
+/* Halo planes: pack the bottom (lo != 0) and top (hi != 0) node planes of y
+ * into send = [lo plane: 3 x plane][hi plane: 3 x plane]; unpack adds the
+ * neighbours' partial sums (same layout) into y's planes and, for mode 1,
+ * re-applies the constraint convention there using THIS context's fixed
+ * flags: fixed entries take vfix[i] (Hessian action: v, operator.py:417) or
+ * cfix when vfix is NULL (diagonal: 1.0, operator.py:458); mode 0 keeps the
+ * sum (gradient: 0 + 0).  nn must equal the context's node count. */
+int tmop_halo_pack(tmop_ctx *ctx, int64_t nn, int64_t plane, int lo, int hi, const double *y, double *send);
+int tmop_halo_unpack(tmop_ctx *ctx, int64_t nn, int64_t plane, int lo, int hi, const double *recv, int mode,
+                     const double *vfix, double cfix, double *y);
 
 #ifdef __cplusplus
 }

@@ -443,13 +443,19 @@ class OQData:
         return coeffs, pl(self.S).copy(), pl(self.T).copy()
 
 
+def _pt(a):
+    """Broadcast a per-point (Ne, Q) factor over (Ne, Q, d, d); scalars pass."""
+    a = np.asarray(a, float)
+    return a[..., None, None] if a.ndim else a
+
+
 class OracleProblem:
     """CPU twin of TmopProblem for ideal constant isotropic targets W = s I
     (met:293-345): only inv_scale = 1/s and det_w = s^d reach the kernels."""
 
     def __init__(self, mesh: OMesh, metric: int, n_quad: int, target: str = "unit",
                  h: float | None = None, spatial_weight: float = 1.0,
-                 limiting: dict | None = None):
+                 limiting: dict | None = None, size=None):
         need = METRIC_DIM[metric]
         if need is not None and need != mesh.dim:
             raise ValueError("metric/dimension mismatch")
@@ -457,6 +463,22 @@ class OracleProblem:
         self.mesh = mesh
         self.metric = metric
         self.omega = spatial_weight
+        if target == "field":
+            # size-field targets (EXTENSION -- no reference code: parity
+            # unpinned; metrics.py:282-345 has constant W only): W_q =
+            # v_q^(1/d) I, v_q = B-interpolated nodal target volume; the
+            # scales become (Ne, Q) arrays (material field, fixed per point)
+            D = self.disc
+            U = D.gather(np.asarray(size, float)[None, :])[0]
+            vq = _fwd(U, [D.B] * mesh.dim).reshape(mesh.n_elements, D.Q)
+            if not np.all(vq > 0):
+                raise ValueError("size field: non-positive target volume at a quadrature point")
+            isq = 1.0 / np.cbrt(vq) if mesh.dim == 3 else 1.0 / np.sqrt(vq)
+            self.scale = 1.0 / isq
+            self.inv_scale = isq
+            self.det_w = 1.0 / isq ** mesh.dim
+            self.limiting = None
+            return
         if target == "unit":
             scale = 1.0
         elif h is not None:
@@ -485,7 +507,7 @@ class OracleProblem:
         if dj.flat[k] <= 0.0:
             e, q = divmod(k, self.disc.Q)
             raise InvalidMesh(e, q, dj.flat[k])
-        return J * self.inv_scale
+        return J * _pt(self.inv_scale)
 
     # -- ProblemLike
     def min_det_jacobian(self, x):
@@ -494,7 +516,10 @@ class OracleProblem:
     def objective(self, x):
         T = self._checked_T(x)
         mu = metric_value(self.metric, T)
-        F = self.omega * self.det_w * float(np.sum(mu @ self.disc.wq))
+        if np.ndim(self.det_w):
+            F = self.omega * float(np.sum((self.det_w * mu) @ self.disc.wq))
+        else:
+            F = self.omega * self.det_w * float(np.sum(mu @ self.disc.wq))
         if self.limiting is not None:
             F += self.limiting_value(x)
         return F
@@ -502,7 +527,7 @@ class OracleProblem:
     def gradient(self, x):
         T = self._checked_T(x)
         coef = self.omega * self.det_w * self.inv_scale
-        P = metric_first(self.metric, T) * (coef * self.disc.wq)[None, :, None, None]
+        P = metric_first(self.metric, T) * _pt(coef * self.disc.wq[None, :])
         out = self.disc.pull_back(P)
         if self.limiting is not None:
             out += self._lim_grad2(self._x2(x))
@@ -514,6 +539,7 @@ class OracleProblem:
         tau = det(T)
         S = cofactor(T) / tau[..., None, None]
         w = (self.omega * self.det_w * self.inv_scale ** 2) * np.broadcast_to(self.disc.wq, tau.shape)
+        w = np.broadcast_to(w, tau.shape)
         c = None
         if self.metric in TEMPLATE_METRICS:
             c = np.stack(second_coeffs(self.metric, tau, frob2(T)), axis=-1) * w[..., None]
@@ -604,8 +630,8 @@ class OracleProblem:
         D, mesh = self.disc, self.mesh
         d = mesh.dim
         T = self._checked_T(x)
-        H = metric_second(self.metric, T) * (self.omega * self.det_w * self.inv_scale ** 2
-                                             * D.wq)[None, :, None, None]
+        H = metric_second(self.metric, T) * _pt(self.omega * self.det_w * self.inv_scale ** 2
+                                                * D.wq[None, :])
         # dense gradient tables grads[q, i, b]
         Np = D.n ** d
         eye = np.eye(Np).reshape((Np,) + (D.n,) * d)

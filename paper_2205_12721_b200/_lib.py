@@ -45,6 +45,8 @@ _SIGS = {
     "tmop_ctx_set_stream": [_P, _P],
     "tmop_ctx_set_apply_overlap": [_P, _INT, _I64],
     "tmop_ctx_set_target": [_P, _D, _D],
+    "tmop_ctx_set_size_field": [_P, _P],
+    "tmop_ctx_point_scale": [_P],
     "tmop_ctx_set_lattice": [_P, _INT, _INT, _INT, _P],
     "tmop_hessian_apply_elements_range": [_P, _P, _P, _I64, _I64],
     "tmop_hessian_apply_gather_range": [_P, _P, _P, _I64, _I64],
@@ -77,9 +79,17 @@ _SIGS = {
     "tmop_minres_step": [_P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _D, _P, _INT],
     "tmop_minres_set_history": [_P, _P, _INT],
     "tmop_minres_step_op": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _D, _P, _INT],
+    "tmop_minres_dist_init_a": [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "tmop_minres_dist_init_b": [_P, _I64, _P, _P, _P, _P],
+    "tmop_minres_dist_k1": [_P, _I64, _I64, _I64, _P, _P, _P, _P, _INT, _P],
+    "tmop_minres_dist_k2": [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _INT, _P],
+    "tmop_minres_dist_k3": [_P, _I64, _P, _P, _P, _P, _P, _P, _D, _P, _INT, _P],
+    "tmop_halo_pack": [_P, _I64, _I64, _INT, _INT, _P, _P],
+    "tmop_halo_unpack": [_P, _I64, _I64, _INT, _INT, _P, _INT, _P, _D, _P],
     "tmop_last_error": [],
 }
-_RESTYPES = {"tmop_qdata_size": _I64, "tmop_qdata_stride": _I64, "tmop_last_error": C.c_char_p}
+_RESTYPES = {"tmop_qdata_size": _I64, "tmop_qdata_stride": _I64, "tmop_last_error": C.c_char_p,
+             "tmop_ctx_point_scale": _P}
 
 EXPORTED = tuple(_SIGS)
 

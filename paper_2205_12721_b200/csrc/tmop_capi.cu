@@ -67,6 +67,8 @@ struct tmop_ctx {
   cudaEvent_t ev[33];
   int ov_slabs;
   int64_t ov_min;    // fewest elements for the overlapped path
+  double *tscale;    // size-field targets: per-point 1 / s_q (NULL: constant target)
+  double *tscale_buf;
   double *hist;      // MINRES residual history (device, optional)
   int hist_cap;
 };
@@ -123,6 +125,8 @@ static ElemArgs base_args(const tmop_ctx *c) {
   a.part_sum = c->part_sum;
   a.part_min = c->part_min;
   a.part_arg = c->part_arg;
+  a.tscale = c->tscale;
+  a.omega = c->omega;
   return a;
 }
 
@@ -273,6 +277,7 @@ int tmop_ctx_destroy(tmop_ctx *c) {
     for (int i = 0; i < 33; ++i) cudaEventDestroy(c->ev[i]);
     cudaStreamDestroy(c->s2);
   }
+  cudaFree(c->tscale_buf);
   cudaFree(c->E2);
   cudaFree(c->lim_y);
   cudaFree(c->lim_val);
@@ -332,8 +337,33 @@ int tmop_ctx_set_target(tmop_ctx *c, double inv_scale, double det_w) {
   if (!(inv_scale > 0.0) || !(det_w > 0.0)) return fail(TMOP_ERR_ARG, "target scale must be positive");
   c->inv_s = inv_scale;
   c->det_w = det_w;
+  c->tscale = nullptr;   // a constant target replaces a size field
   return TMOP_OK;
 }
+
+int tmop_ctx_set_size_field(tmop_ctx *c, const double *volume_nodal) {
+  if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
+  if (!volume_nodal) {
+    c->tscale = nullptr;
+    c->inv_s = c->det_w = 1.0;
+    return TMOP_OK;
+  }
+  if (c->lim_on) return fail(TMOP_ERR_ARG, "size-field targets are not combined with the limiting term");
+  const int64_t qp = c->dim == 3 ? (int64_t)c->nq * c->nq * c->nq : (int64_t)c->nq * c->nq;
+  if (!c->tscale_buf) CUDA_TRY(cudaMalloc(&c->tscale_buf, (size_t)(c->ne * qp > 0 ? c->ne * qp : 1) * sizeof(double)));
+  c->tscale = nullptr;
+  c->inv_s = c->det_w = 1.0;
+  ElemArgs a = base_args(c);
+  a.lim_dn = volume_nodal;
+  a.qout = c->tscale_buf;
+  const int g = launch_elem(c->dim, c->n1, c->nq, K_TSCALE, a, c->tab, c->stream);
+  if (g < 0) return fail(TMOP_ERR_ARG, "no size-field kernel for dim=%d p=%d n_q=%d", c->dim, c->order, c->nq);
+  CUDA_TRY(cudaGetLastError());
+  c->tscale = c->tscale_buf;
+  return TMOP_OK;
+}
+
+const double *tmop_ctx_point_scale(const tmop_ctx *c) { return c ? c->tscale : nullptr; }
 
 int tmop_qdata_fields(const tmop_ctx *c) {
   if (!c) return -1;
@@ -377,6 +407,7 @@ int tmop_ctx_set_limiting(tmop_ctx *c, const double *x0, const double *delta_nod
     return TMOP_OK;
   }
   if (!(weight > 0.0)) return fail(TMOP_ERR_ARG, "limiting weight must be positive");
+  if (c->tscale) return fail(TMOP_ERR_ARG, "the limiting term is not combined with size-field targets");
   if (!delta_nodal && !(delta > 0.0)) return fail(TMOP_ERR_ARG, "limiting delta must be positive");
   if (!c->E2) {
     const size_t esz = (size_t)(c->ne > 0 ? c->ne : 1) * c->dim * c->NP;
@@ -691,6 +722,79 @@ int tmop_minres_step(tmop_ctx *c, int64_t n, double *Av, const double *r1, const
   if (!c || !st2) return fail(TMOP_ERR_ARG, "NULL argument");
   launch_minres_step(n, Av, r1, r2, inv, z, v, w, w1buf, w2, x, rtol, st2 + (k & 1), st2 + ((k + 1) & 1), c->vpart1,
                      c->vpart2, c->hist, c->hist_cap, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+// ---- slab-partitioned MINRES (see tmop_b200.h) ----
+static int dist_args_ok(tmop_ctx *c, int64_t n, int64_t nn, int64_t n_owned, const void *scal) {
+  if (!c || !scal) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (nn < 0 || n_owned < 0 || n_owned > nn || (nn && n % nn))
+    return fail(TMOP_ERR_ARG, "owned range invalid (n %lld, nn %lld, n_owned %lld)", (long long)n, (long long)nn,
+                (long long)n_owned);
+  return TMOP_OK;
+}
+
+int tmop_minres_dist_init_a(tmop_ctx *c, int64_t n, int64_t nn, int64_t n_owned, const double *b, const double *inv,
+                            double *x, double *r1, double *r2, double *z, double *w, double *w2, double *scal) {
+  int rc = dist_args_ok(c, n, nn, n_owned, scal);
+  if (rc) return rc;
+  launch_minres_dist_init_a(n, nn, n_owned, b, inv, x, r1, r2, z, w, w2, c->vpart1, scal, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_minres_dist_init_b(tmop_ctx *c, int64_t n, const double *z, double *v, const double *scal,
+                            tmop_minres_state *st2) {
+  if (!c || !scal || !st2) return fail(TMOP_ERR_ARG, "NULL argument");
+  launch_minres_dist_init_b(n, z, v, scal, st2, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_minres_dist_k1(tmop_ctx *c, int64_t n, int64_t nn, int64_t n_owned, double *Av, const double *r1,
+                        const double *v, tmop_minres_state *st2, int k, double *scal) {
+  int rc = dist_args_ok(c, n, nn, n_owned, scal);
+  if (rc) return rc;
+  if (!st2) return fail(TMOP_ERR_ARG, "NULL state");
+  launch_minres_dist_k1(n, nn, n_owned, Av, r1, v, st2 + (k & 1), c->vpart1, scal, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_minres_dist_k2(tmop_ctx *c, int64_t n, int64_t nn, int64_t n_owned, double *Av, const double *r2,
+                        const double *inv, double *z, tmop_minres_state *st2, int k, double *scal) {
+  int rc = dist_args_ok(c, n, nn, n_owned, scal);
+  if (rc) return rc;
+  if (!st2) return fail(TMOP_ERR_ARG, "NULL state");
+  launch_minres_dist_k2(n, nn, n_owned, Av, r2, inv, z, st2 + (k & 1), c->vpart2, scal, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_minres_dist_k3(tmop_ctx *c, int64_t n, const double *z, double *v, const double *w, double *w1buf,
+                        const double *w2, double *x, double rtol, tmop_minres_state *st2, int k, const double *scal) {
+  if (!c || !scal || !st2) return fail(TMOP_ERR_ARG, "NULL argument");
+  launch_minres_dist_k3(n, z, v, w, w1buf, w2, x, rtol, st2 + (k & 1), st2 + ((k + 1) & 1), scal, c->hist,
+                        c->hist_cap, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_halo_pack(tmop_ctx *c, int64_t nn, int64_t plane, int lo, int hi, const double *y, double *send) {
+  if (!c || !y || !send) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (plane < 0 || 2 * plane > nn + plane) return fail(TMOP_ERR_ARG, "plane size invalid");
+  launch_halo_pack(nn, plane, lo, hi, y, send, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_halo_unpack(tmop_ctx *c, int64_t nn, int64_t plane, int lo, int hi, const double *recv, int mode,
+                     const double *vfix, double cfix, double *y) {
+  if (!c || !y || !recv) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (nn != c->nn) return fail(TMOP_ERR_ARG, "node count %lld does not match the context (%lld)", (long long)nn,
+                               (long long)c->nn);
+  launch_halo_unpack(nn, plane, lo, hi, recv, c->fixed, mode, vfix, cfix, y, c->stream);
   CUDA_TRY(cudaGetLastError());
   return TMOP_OK;
 }

@@ -1,6 +1,7 @@
 // tmop_core.cu -- mesh-level kernels: deterministic E->L gather-sum, the
 // fixed-order finalisation of per-CTA partials, pointwise metric
 // evaluation, and the fused vector kernels of the device MINRES.
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -332,6 +333,18 @@ void launch_jacobi(int64_t n, const double *d, double fl, double *inv, int32_t *
 }
 
 // ------------------------------------------------------------- MINRES
+// Dot products of a slab partition count each shared node plane once: entry
+// i of a component-major (D, nn) local vector is OWNED when its node
+// (i mod nn) < n_owned.  nn == 0: every entry is owned (single GPU).
+struct Own {
+  int64_t nn, n_owned;
+  __device__ __forceinline__ bool operator()(int64_t i) const {
+    if (nn == 0) return true;
+    while (i >= nn) i -= nn;
+    return i < n_owned;
+  }
+};
+
 // Reference recurrence: solvers.py:117-178.  Scalars live in device
 // memory; two state slots alternate by iteration parity so that the CTAs of
 // the last fused kernel can all read the old state while CTA 0 writes the
@@ -339,7 +352,7 @@ void launch_jacobi(int64_t n, const double *d, double fl, double *inv, int32_t *
 __global__ void __launch_bounds__(VEC_NT) minres_init_kernel(int64_t n, const double *__restrict__ b,
                                                              const double *__restrict__ inv, double *x, double *r1,
                                                              double *r2, double *z, double *w, double *w2,
-                                                             double *__restrict__ part) {
+                                                             double *__restrict__ part, const Own own) {
   __shared__ double sv[VEC_NT / 32];
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT) {
@@ -351,7 +364,7 @@ __global__ void __launch_bounds__(VEC_NT) minres_init_kernel(int64_t n, const do
     x[i] = 0.0;
     w[i] = 0.0;
     w2[i] = 0.0;
-    s += bi * zi;
+    if (own(i)) s += bi * zi;
   }
   s = block_sum<VEC_NT>(s, sv);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -392,7 +405,7 @@ __global__ void __launch_bounds__(VEC_NT) minres_init2_kernel(int64_t n, const d
 // K1: Av -= (beta/oldb) r1 (itn >= 2); partial alfa = v . Av
 __global__ void __launch_bounds__(VEC_NT) minres_k1(int64_t n, double *__restrict__ Av, const double *__restrict__ r1,
                                                     const double *__restrict__ v, const tmop_minres_state *cur,
-                                                    double *__restrict__ part) {
+                                                    double *__restrict__ part, const Own own) {
   if (cur->done) return;
   __shared__ double sv[VEC_NT / 32];
   const bool sub = cur->itn >= 1;
@@ -404,7 +417,7 @@ __global__ void __launch_bounds__(VEC_NT) minres_k1(int64_t n, double *__restric
       y = y - f * r1[i];
       Av[i] = y;
     }
-    s += v[i] * y;
+    if (own(i)) s += v[i] * y;
   }
   s = block_sum<VEC_NT>(s, sv);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -417,7 +430,7 @@ template <bool V2>
 __global__ void __launch_bounds__(VEC_NT) minres_k2(int64_t n, double *__restrict__ Av, const double *__restrict__ r2,
                                                     const double *__restrict__ inv, double *__restrict__ z,
                                                     const tmop_minres_state *cur, const double *__restrict__ part1,
-                                                    int np1, double *__restrict__ part2) {
+                                                    int np1, double *__restrict__ part2, const Own own) {
   if (cur->done) return;
   __shared__ double sv[VEC_NT / 32];
   const double alfa = reduce_partials(part1, np1, sv);
@@ -428,7 +441,7 @@ __global__ void __launch_bounds__(VEC_NT) minres_k2(int64_t n, double *__restric
     Av[i] = y;
     const double zi = inv ? inv[i] * y : y;
     z[i] = zi;
-    s += y * zi;
+    if (own(i)) s += y * zi;
   };
   const int64_t gid = (int64_t)blockIdx.x * VEC_NT + threadIdx.x, stride = (int64_t)gridDim.x * VEC_NT;
   if constexpr (V2) {
@@ -446,8 +459,8 @@ __global__ void __launch_bounds__(VEC_NT) minres_k2(int64_t n, double *__restric
         zz = y;
       }
       reinterpret_cast<double2 *>(z)[j] = zz;
-      s += y.x * zz.x;
-      s += y.y * zz.y;
+      if (own(2 * j)) s += y.x * zz.x;
+      if (own(2 * j + 1)) s += y.y * zz.y;
     }
     if (gid == 0 && (n & 1)) one(n - 1);
   } else {
@@ -543,7 +556,7 @@ __global__ void __launch_bounds__(VEC_NT) minres_k3(int64_t n, const double *__r
 void launch_minres_init(int64_t n, const double *b, const double *inv, double *x, double *r1, double *r2, double *z,
                         double *v, double *w, double *w2, double *part, tmop_minres_state *st, cudaStream_t s) {
   const int g = vec_grid(n);
-  minres_init_kernel<<<g, VEC_NT, 0, s>>>(n, b, inv, x, r1, r2, z, w, w2, part);
+  minres_init_kernel<<<g, VEC_NT, 0, s>>>(n, b, inv, x, r1, r2, z, w, w2, part, Own{0, 0});
   minres_init2_kernel<<<g, VEC_NT, 0, s>>>(n, z, v, part, g, st);
 }
 
@@ -556,11 +569,11 @@ static void launch_k23(int64_t n, double *Av, const double *r2, const double *in
   const bool v2 = al16(Av) && al16(r2) && (!inv || al16(inv)) && al16(z) && al16(v) && al16(w) && al16(w1buf) &&
                   al16(w2) && al16(x);
   if (v2) {
-    minres_k2<true><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, np1, part2);
+    minres_k2<true><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, np1, part2, Own{0, 0});
     minres_k3<true><<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, np1, part2, g, rtol, hist,
                                          hist_cap);
   } else {
-    minres_k2<false><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, np1, part2);
+    minres_k2<false><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, part1, np1, part2, Own{0, 0});
     minres_k3<false><<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, part1, np1, part2, g, rtol, hist,
                                           hist_cap);
   }
@@ -638,8 +651,104 @@ void launch_minres_step(int64_t n, double *Av, const double *r1, const double *r
                         tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, double *part2,
                         double *hist, int hist_cap, cudaStream_t s) {
   const int g = vec_grid(n);
-  minres_k1<<<g, VEC_NT, 0, s>>>(n, Av, r1, v, cur, part1);
+  minres_k1<<<g, VEC_NT, 0, s>>>(n, Av, r1, v, cur, part1, Own{0, 0});
   launch_k23(n, Av, r2, inv, z, v, w, w1buf, w2, x, rtol, cur, nxt, part1, g, part2, hist, hist_cap, g, s);
+}
+
+// ---- slab-partitioned MINRES phases (tmop_minres_dist_*): every phase that
+// ends in a dot product reduces its owned-entry partials in a fixed order
+// into scal[k]; the caller all-reduces scal[k] across ranks in between, and
+// the next phase reads the global value as a one-entry partial array.
+void launch_minres_dist_init_a(int64_t n, int64_t nn, int64_t n_owned, const double *b, const double *inv, double *x,
+                               double *r1, double *r2, double *z, double *w, double *w2, double *part, double *scal,
+                               cudaStream_t s) {
+  const int g = vec_grid(n);
+  minres_init_kernel<<<g, VEC_NT, 0, s>>>(n, b, inv, x, r1, r2, z, w, w2, part, Own{nn, n_owned});
+  sum_partials_kernel<<<1, VEC_NT, 0, s>>>(g, part, scal);
+}
+
+void launch_minres_dist_init_b(int64_t n, const double *z, double *v, const double *scal, tmop_minres_state *st,
+                               cudaStream_t s) {
+  minres_init2_kernel<<<vec_grid(n), VEC_NT, 0, s>>>(n, z, v, scal, 1, st);
+}
+
+void launch_minres_dist_k1(int64_t n, int64_t nn, int64_t n_owned, double *Av, const double *r1, const double *v,
+                           const tmop_minres_state *cur, double *part, double *scal, cudaStream_t s) {
+  const int g = vec_grid(n);
+  minres_k1<<<g, VEC_NT, 0, s>>>(n, Av, r1, v, cur, part, Own{nn, n_owned});
+  sum_partials_kernel<<<1, VEC_NT, 0, s>>>(g, part, scal);
+}
+
+void launch_minres_dist_k2(int64_t n, int64_t nn, int64_t n_owned, double *Av, const double *r2, const double *inv,
+                           double *z, const tmop_minres_state *cur, double *part, double *scal, cudaStream_t s) {
+  const int g = vec_grid(n);
+  const bool v2 = al16(Av) && al16(r2) && (!inv || al16(inv)) && al16(z);
+  if (v2)
+    minres_k2<true><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, scal, 1, part, Own{nn, n_owned});
+  else
+    minres_k2<false><<<g, VEC_NT, 0, s>>>(n, Av, r2, inv, z, cur, scal, 1, part, Own{nn, n_owned});
+  sum_partials_kernel<<<1, VEC_NT, 0, s>>>(g, part, scal + 1);
+}
+
+void launch_minres_dist_k3(int64_t n, const double *z, double *v, const double *w, double *w1buf, const double *w2,
+                           double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt,
+                           const double *scal, double *hist, int hist_cap, cudaStream_t s) {
+  const int g = vec_grid(n);
+  const bool v2 = al16(z) && al16(v) && al16(w) && al16(w1buf) && al16(w2) && al16(x);
+  if (v2)
+    minres_k3<true><<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, scal, 1, scal + 1, 1, rtol, hist,
+                                         hist_cap);
+  else
+    minres_k3<false><<<g, VEC_NT, 0, s>>>(n, z, v, w, w1buf, w2, x, cur, nxt, scal, 1, scal + 1, 1, rtol, hist,
+                                          hist_cap);
+}
+
+// Shared node planes of a z-slab (component-major local vector (3, nn); the
+// planes are nodes [0, pl) and [nn - pl, nn)): pack both into one send
+// buffer [lo: 3 pl][hi: 3 pl] ...
+__global__ void halo_pack_kernel(int64_t nn, int64_t pl, int lo, int hi, const double *__restrict__ y,
+                                 double *__restrict__ send) {
+  const int64_t tot = 3 * pl;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / pl, j = i - c * pl;
+    if (lo) send[i] = y[c * nn + j];
+    if (hi) send[tot + i] = y[c * nn + nn - pl + j];
+  }
+}
+
+// ... and add the neighbours' partial sums back, re-applying the constraint
+// convention on those planes (operator.py:417 / :458): fixed entries take
+// vfix[i] (the apply's v) or cfix (the diagonal's 1.0) when vfix == NULL;
+// mode 0 leaves fixed entries as summed (the gradient's 0 + 0).
+__global__ void halo_unpack_kernel(int64_t nn, int64_t pl, int lo, int hi, const double *__restrict__ recv,
+                                   const uint8_t *__restrict__ fixed, int mode, const double *__restrict__ vfix,
+                                   double cfix, double *__restrict__ y) {
+  const int64_t tot = 3 * pl;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / pl, j = i - c * pl;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      if (side == 0 ? !lo : !hi) continue;
+      const int64_t node = side == 0 ? j : nn - pl + j;
+      const int64_t k = c * nn + node;
+      double val = y[k] + recv[side * tot + i];
+      if (mode && ((__ldg(fixed + node) >> c) & 1)) val = vfix ? vfix[k] : cfix;
+      y[k] = val;
+    }
+  }
+}
+
+void launch_halo_pack(int64_t nn, int64_t pl, int lo, int hi, const double *y, double *send, cudaStream_t s) {
+  const int64_t tot = 3 * pl;
+  const int g = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+  if (g > 0) halo_pack_kernel<<<g, 256, 0, s>>>(nn, pl, lo, hi, y, send);
+}
+
+void launch_halo_unpack(int64_t nn, int64_t pl, int lo, int hi, const double *recv, const uint8_t *fixed, int mode,
+                        const double *vfix, double cfix, double *y, cudaStream_t s) {
+  const int64_t tot = 3 * pl;
+  const int g = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+  if (g > 0) halo_unpack_kernel<<<g, 256, 0, s>>>(nn, pl, lo, hi, recv, fixed, mode, vfix, cfix, y);
 }
 
 }  // namespace tmop

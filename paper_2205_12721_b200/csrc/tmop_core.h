@@ -59,6 +59,21 @@ void launch_minres_k23(int64_t n, double *Av, const double *r2, const double *in
                        const double *w, double *w1buf, const double *w2, double *x, double rtol,
                        tmop_minres_state *cur, tmop_minres_state *nxt, double *part1, int np1, double *part2,
                        double *hist, int hist_cap, cudaStream_t s);
+void launch_minres_dist_init_a(int64_t n, int64_t nn, int64_t n_owned, const double *b, const double *inv, double *x,
+                               double *r1, double *r2, double *z, double *w, double *w2, double *part, double *scal,
+                               cudaStream_t s);
+void launch_minres_dist_init_b(int64_t n, const double *z, double *v, const double *scal, tmop_minres_state *st,
+                               cudaStream_t s);
+void launch_minres_dist_k1(int64_t n, int64_t nn, int64_t n_owned, double *Av, const double *r1, const double *v,
+                           const tmop_minres_state *cur, double *part, double *scal, cudaStream_t s);
+void launch_minres_dist_k2(int64_t n, int64_t nn, int64_t n_owned, double *Av, const double *r2, const double *inv,
+                           double *z, const tmop_minres_state *cur, double *part, double *scal, cudaStream_t s);
+void launch_minres_dist_k3(int64_t n, const double *z, double *v, const double *w, double *w1buf, const double *w2,
+                           double *x, double rtol, tmop_minres_state *cur, tmop_minres_state *nxt,
+                           const double *scal, double *hist, int hist_cap, cudaStream_t s);
+void launch_halo_pack(int64_t nn, int64_t pl, int lo, int hi, const double *y, double *send, cudaStream_t s);
+void launch_halo_unpack(int64_t nn, int64_t pl, int lo, int hi, const double *recv, const uint8_t *fixed, int mode,
+                        const double *vfix, double cfix, double *y, cudaStream_t s);
 int launch_lattice_check(int64_t ne, int np, const int32_t *restr, int nx, int ny, int nz, int p, int *flag,
                          cudaStream_t s);
 

@@ -41,7 +41,8 @@ enum Kind : int {
   K_LIM_VALUE = 10,  // limiting_value        (operator.py:488-495)
   K_LIM_FIELD = 11,  // limiting gradient / Hessian action (operator.py:497-533)
   K_LIM_DIAG = 12,   // limiting part of hessian_diagonal (operator.py:452-457)
-  K_COUNT = 13
+  K_TSCALE = 13,     // size-field targets: per-point 1/scale from a nodal target volume (extension)
+  K_COUNT = 14
 };
 
 // Tuning knobs (compile-time overrides for tools/build_variant.sh; 0 = the
@@ -183,7 +184,40 @@ struct ElemArgs {
   int lim_mask;       // zero constrained input components (hessian_apply)
   int energy;         // K_GRAD: also accumulate the energy into part_sum
   const int32_t *stop;   // if non-NULL and *stop != 0 the launch is a no-op (converged MINRES)
+  // size-field targets (extension; metrics.py:282-345 has constant W only):
+  // W_q = s_q I with tscale[e * QP + q] = 1 / s_q (reference point order);
+  // NULL = the constant target above.  When set, the context passes
+  // inv_s = det_w = 1 and the per-point factors come from PtScale.
+  const double *__restrict__ tscale;
+  double omega;       // spatial weight
 };
+
+// Target factors of one quadrature point (k = e * QP + q): the constant
+// target's uniform values, or the size field's s_q^-1 with det W_q = s_q^d.
+struct PtScale {
+  double is, is_dm1, is_d, cg, ch, ew;
+};
+template <int DIM>
+__device__ __forceinline__ PtScale pt_scale(const ElemArgs &a, int64_t k) {
+  PtScale s;
+  if (a.tscale == nullptr) {
+    s.is = a.inv_s;
+    s.is_dm1 = a.inv_s_dm1;
+    s.is_d = a.inv_s_d;
+    s.cg = a.coef_g;
+    s.ch = a.coef_h;
+    s.ew = 1.0;
+    return s;
+  }
+  const double is = __ldg(a.tscale + k);
+  s.is = is;
+  s.is_dm1 = DIM == 3 ? is * is : is;
+  s.is_d = s.is_dm1 * is;
+  s.ew = 1.0 / s.is_d;              // det W_q (energy weight; coef_e = omega)
+  s.cg = a.omega * s.ew * is;       // omega det_w inv_s   (operator.py:330)
+  s.ch = s.cg * is;                 // omega det_w inv_s^2 (operator.py:358-359)
+  return s;
+}
 
 // Point slot of quadrature point q (x fastest, fe.py:134-140) inside a lean
 // Q-data field: 3D records store qx as the SLOWEST index (slot = line +
@@ -725,10 +759,11 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::template m
           mn = minloc(mn, MinLoc{dj, eg * QP + q});
         }
         if constexpr (KIND == K_SETUP || KIND == K_GRAD || KIND == K_ENERGY) {
-          const double tau = dj * a.inv_s_d;
-          const double I1 = mfro2<DIM>(A) * (a.inv_s * a.inv_s);
+          const PtScale ps = pt_scale<DIM>(a, eg * QP + q);
+          const double tau = dj * ps.is_d;
+          const double I1 = mfro2<DIM>(A) * (ps.is * ps.is);
           const double itau = 1.0 / tau;   // the one division of the point
-          const double cs = a.inv_s_dm1 * itau;
+          const double cs = ps.is_dm1 * itau;
           double Cof[DIM][DIM];
           mcof<DIM>(A, Cof);
           double S[DIM][DIM], T[DIM][DIM];
@@ -737,32 +772,32 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::template m
 #pragma unroll
             for (int j = 0; j < DIM; ++j) {
               S[i][j] = cs * Cof[i][j];
-              T[i][j] = a.inv_s * A[i][j];
+              T[i][j] = ps.is * A[i][j];
             }
           const double wpt = wq<DIM, Q>(t, q);
           if constexpr (KIND == K_ENERGY) {
-            acc += wpt * metric_mu<DIM>(a.metric, tau, I1, S);
+            acc += (wpt * ps.ew) * metric_mu<DIM>(a.metric, tau, I1, S);
           } else if constexpr (KIND == K_SETUP) {
             // lean record (operator.py:350-371 restated; see lean_k0)
             double *qo = a.qout + eg * QS + lean_slot<DIM, Q>(q);
             store_point<DIM>(qo, QP, T);
-            qo[DIM * DIM * QP] = lean_k0(a.metric, a.coef_h * wpt, tau);
+            qo[DIM * DIM * QP] = lean_k0(a.metric, ps.ch * wpt, tau);
             qo[(DIM * DIM + 1) * QP] = itau;
           } else {  // K_GRAD (+ the energy, for the fused line-search evaluation)
-            const double cw = a.coef_g * wpt;
+            const double cw = ps.cg * wpt;
             double P[DIM][DIM];
             if (metric_is_template(a.metric)) {
               double at, as, mu = 0.0;
               metric_mu_first<DIM>(a.metric, tau, I1, S, a.energy, mu, at, as);
-              if (a.energy) acc += wpt * mu;
-              const double ct = cw * at * a.inv_s;
-              const double cc = cw * as * a.inv_s_dm1 * itau;
+              if (a.energy) acc += (wpt * ps.ew) * mu;
+              const double ct = cw * at * ps.is;
+              const double cc = cw * as * ps.is_dm1 * itau;
 #pragma unroll
               for (int i = 0; i < DIM; ++i)
 #pragma unroll
                 for (int j = 0; j < DIM; ++j) P[i][j] = ct * A[i][j] + cc * Cof[i][j];
             } else {
-              if (a.energy) acc += wpt * metric_mu<DIM>(a.metric, tau, I1, S);
+              if (a.energy) acc += (wpt * ps.ew) * metric_mu<DIM>(a.metric, tau, I1, S);
               nt_first<DIM>(a.metric, T, S, P);
 #pragma unroll
               for (int i = 0; i < DIM; ++i)

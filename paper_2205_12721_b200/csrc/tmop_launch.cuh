@@ -101,7 +101,7 @@ int launch_lim(ElemArgs &a, const Tab &t, cudaStream_t s) {
 template <int DIM, int N, int Q, int KIND>
 int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
   using CF = Cfg<DIM, N, Q>;
-  if constexpr (KIND == K_LIM_VALUE || KIND == K_LIM_FIELD || KIND == K_LIM_DIAG) {
+  if constexpr (KIND == K_LIM_VALUE || KIND == K_LIM_FIELD || KIND == K_LIM_DIAG || KIND == K_TSCALE) {
     return launch_lim<DIM, N, Q, KIND>(a, t, s);
   } else if constexpr (KIND == K_DIAG || KIND == K_DIAG_NT) {
     return launch_diag<DIM, N, Q, KIND == K_DIAG_NT>(a, t, s);
@@ -140,6 +140,7 @@ int launch_kind(int kind, ElemArgs &a, const Tab &t, cudaStream_t s) {
     case K_LIM_VALUE: return launch_one<DIM, N, Q, K_LIM_VALUE>(a, t, s);
     case K_LIM_FIELD: return launch_one<DIM, N, Q, K_LIM_FIELD>(a, t, s);
     case K_LIM_DIAG: return launch_one<DIM, N, Q, K_LIM_DIAG>(a, t, s);
+    case K_TSCALE: return launch_one<DIM, N, Q, K_TSCALE>(a, t, s);
     default: return -1;
   }
 }

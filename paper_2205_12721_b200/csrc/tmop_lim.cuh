@@ -70,8 +70,9 @@ __global__ void __launch_bounds__(LimCfg<DIM, N, Q>::NT) lim_kernel(const ElemAr
     TT[i] = KIND == K_LIM_DIAG ? b * b : b;
   }
   const bool nodal = a.lim_dn != nullptr;
-  const int nf = KIND == K_LIM_DIAG ? (nodal ? 1 : 0) : DIM + (nodal ? 1 : 0);
-  const int fd = KIND == K_LIM_DIAG ? 0 : DIM;          // field index of nodal delta
+  // K_TSCALE (size-field targets): the nodal target volume rides in lim_dn
+  const int nf = (KIND == K_LIM_DIAG || KIND == K_TSCALE) ? (nodal ? 1 : 0) : DIM + (nodal ? 1 : 0);
+  const int fd = (KIND == K_LIM_DIAG || KIND == K_TSCALE) ? 0 : DIM;   // field index of the nodal scalar
   double acc = 0.0;
   __syncthreads();
 
@@ -118,6 +119,13 @@ __global__ void __launch_bounds__(LimCfg<DIM, N, Q>::NT) lim_kernel(const ElemAr
       const int e = w / QP, q = w % QP;
       const int64_t eg = e0 + e;
       double *vq = V + e * R + q;
+      if constexpr (KIND == K_TSCALE) {
+        // W_q = v_q^(1/d) I from the interpolated target volume v_q: store 1 / s_q
+        // (NaN marks v_q <= 0, checked by the caller)
+        const double vv = vq[0];
+        if (eg < a.ne) a.qout[eg * QP + q] = vv > 0.0 ? (DIM == 3 ? 1.0 / cbrt(vv) : 1.0 / sqrt(vv)) : NAN;
+        continue;
+      }
       const double dq = nodal ? vq[fd * QP] : a.lim_delta;
       const double cq = (a.lim_base * wq<DIM, Q>(t, q)) / (dq * dq);
       if constexpr (KIND == K_LIM_VALUE) {
@@ -135,7 +143,7 @@ __global__ void __launch_bounds__(LimCfg<DIM, N, Q>::NT) lim_kernel(const ElemAr
       }
     }
     __syncthreads();
-    if constexpr (KIND != K_LIM_VALUE) {
+    if constexpr (KIND != K_LIM_VALUE && KIND != K_TSCALE) {
       // ---- transposed sweeps, x axis first (contract_quad_to_dofs, fe.py:242-253)
       const int nz = KIND == K_LIM_DIAG ? 1 : DIM;
       double *W = (Z == P0) ? P1 : P0;

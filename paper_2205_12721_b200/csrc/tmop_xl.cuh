@@ -251,10 +251,11 @@ __device__ __forceinline__ void xl_point_x(const ElemArgs &a, const Tab &t, int6
   const double dj = mdet<3>(J);
   if (eg < a.ne) mn = minloc(mn, MinLoc{dj, eg * QP + q});
   if constexpr (KIND == K_SETUP || KIND == K_GRAD || KIND == K_ENERGY) {
-    const double tau = dj * a.inv_s_d;
-    const double I1 = mfro2<3>(J) * (a.inv_s * a.inv_s);
+    const PtScale ps = pt_scale<3>(a, (eg < a.ne ? eg : 0) * QP + q);
+    const double tau = dj * ps.is_d;
+    const double I1 = mfro2<3>(J) * (ps.is * ps.is);
     const double itau = 1.0 / tau;   // the one division of the point
-    const double cs = a.inv_s_dm1 * itau;
+    const double cs = ps.is_dm1 * itau;
     double Cof[3][3];
     mcof<3>(J, Cof);
     double S[3][3], T[3][3];
@@ -263,11 +264,11 @@ __device__ __forceinline__ void xl_point_x(const ElemArgs &a, const Tab &t, int6
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         S[i][j] = cs * Cof[i][j];
-        T[i][j] = a.inv_s * J[i][j];
+        T[i][j] = ps.is * J[i][j];
       }
     const double wpt = wq<3, Q>(t, q);
     if constexpr (KIND == K_ENERGY) {
-      if (eg < a.ne) acc += wpt * metric_mu<3>(a.metric, tau, I1, S);
+      if (eg < a.ne) acc += (wpt * ps.ew) * metric_mu<3>(a.metric, tau, I1, S);
     } else if constexpr (KIND == K_SETUP) {
       // lean record (operator.py:350-371 restated; see lean_k0), staged in
       // shared memory at slot = line + Q^2 qx of this thread's element
@@ -276,24 +277,24 @@ __device__ __forceinline__ void xl_point_x(const ElemArgs &a, const Tab &t, int6
       for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j) qo[(i * 3 + j) * QP] = T[i][j];
-      qo[9 * QP] = lean_k0(a.metric, a.coef_h * wpt, tau);
+      qo[9 * QP] = lean_k0(a.metric, ps.ch * wpt, tau);
       qo[10 * QP] = itau;
     } else {  // K_GRAD: P = cw (a_t T + a_s S) (operator.py:328-346), + the energy
-      const double cw = a.coef_g * wpt;
+      const double cw = ps.cg * wpt;
       const bool en = a.energy && eg < a.ne;   // (line-search evaluation)
       double P[3][3];
       if (metric_is_template(a.metric)) {
         double at, as, mu = 0.0;
         metric_mu_first<3>(a.metric, tau, I1, S, en, mu, at, as);
-        if (en) acc += wpt * mu;
-        const double ct = cw * at * a.inv_s;
-        const double cc = cw * as * a.inv_s_dm1 * itau;
+        if (en) acc += (wpt * ps.ew) * mu;
+        const double ct = cw * at * ps.is;
+        const double cc = cw * as * ps.is_dm1 * itau;
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
           for (int j = 0; j < 3; ++j) P[i][j] = ct * J[i][j] + cc * Cof[i][j];
       } else {
-        if (en) acc += wpt * metric_mu<3>(a.metric, tau, I1, S);
+        if (en) acc += (wpt * ps.ew) * metric_mu<3>(a.metric, tau, I1, S);
         nt_first<3>(a.metric, T, S, P);
 #pragma unroll
         for (int i = 0; i < 3; ++i)

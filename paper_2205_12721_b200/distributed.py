@@ -29,7 +29,8 @@ import numpy as np
 
 from .mesh import Mesh, build_box
 
-__all__ = ["SlabPartition", "HaloExchange", "DistributedProblem", "split_layers"]
+__all__ = ["SlabPartition", "HaloExchange", "DistributedProblem", "split_layers", "dist_minres",
+           "dist_minres_device", "dist_newton_solve", "allreduce_"]
 
 
 def _torch():
@@ -119,15 +120,80 @@ def _staged(t, group):
     return t, False
 
 
+def allreduce_(t, op=None, group=None):
+    """In-place all-reduce of a (device) tensor: NCCL keeps it on the stream
+    (no host round trip); gloo stages CUDA tensors through host memory."""
+    import torch.distributed as dist
+    op = dist.ReduceOp.SUM if op is None else op
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+    return t
+
+
 class HaloExchange:
     """Sum of the shared node planes with the z-neighbours (torch.distributed
-    point-to-point, batched; NCCL on GPUs, gloo on CPUs)."""
+    point-to-point, batched; NCCL on GPUs, gloo on CPUs).
 
-    def __init__(self, part: SlabPartition, group=None):
+    With a device TmopProblem (`ctx` given) the planes are packed into one
+    persistent send buffer and unpacked -- neighbour sums added and the
+    constraint convention re-applied on the planes -- by two library kernels
+    (tmop_halo_pack / tmop_halo_unpack); only the NCCL send/recv pair per
+    neighbour sits between them, stream-ordered, no host synchronisation."""
+
+    def __init__(self, part: SlabPartition, group=None, ctx=None, lib=None):
         self.part = part
         self.group = group
         self.bytes_per_exchange = 0
         self.seconds = 0.0
+        self.ctx, self.lib = ctx, lib
+        self._bufs = None
+
+    def _device_bufs(self, like):
+        torch = _torch()
+        if self._bufs is None or self._bufs[0].device != like.device:
+            m = 6 * self.part.plane
+            self._bufs = (torch.empty(m, dtype=torch.float64, device=like.device),
+                          torch.zeros(m, dtype=torch.float64, device=like.device))
+        return self._bufs
+
+    def sum_planes_device(self, y, mode, vfix=None, cfix=0.0):
+        """Device fast path: y (local T-vector on the GPU) receives the
+        neighbours' partial sums on its planes; mode 1 re-fixes constrained
+        entries there to vfix (Hessian action: v) or cfix (diagonal: 1.0),
+        mode 0 leaves them (gradient: 0 + 0)."""
+        import torch.distributed as dist
+
+        from . import _lib
+        pt = self.part
+        lo, hi = int(pt.has_lower), int(pt.has_upper)
+        if not (lo or hi):
+            return y
+        send, recv = self._device_bufs(y)
+        pl = pt.plane
+        _lib.check(self.lib.tmop_halo_pack(self.ctx, pt.n_local, pl, lo, hi, _lib.ptr(y), _lib.ptr(send)),
+                   "tmop_halo_pack")
+        gloo = dist.get_backend(self.group) == "gloo"
+        s_h, r_h = (send.cpu(), recv.cpu()) if gloo else (send, recv)
+        ops = []
+        if lo:
+            ops += [dist.P2POp(dist.isend, s_h[:3 * pl], pt.rank - 1, self.group),
+                    dist.P2POp(dist.irecv, r_h[:3 * pl], pt.rank - 1, self.group)]
+        if hi:
+            ops += [dist.P2POp(dist.isend, s_h[3 * pl:], pt.rank + 1, self.group),
+                    dist.P2POp(dist.irecv, r_h[3 * pl:], pt.rank + 1, self.group)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        if gloo:
+            recv.copy_(r_h)
+        self.bytes_per_exchange = 3 * pl * 8
+        _lib.check(self.lib.tmop_halo_unpack(self.ctx, pt.n_local, pl, lo, hi, _lib.ptr(recv), int(mode),
+                                             _lib.ptr(vfix) if vfix is not None else None, float(cfix),
+                                             _lib.ptr(y)), "tmop_halo_unpack")
+        return y
 
     def sum_planes(self, y):
         """y: local T-vector (3 * n_local); the bottom / top planes receive the
@@ -212,7 +278,11 @@ class DistributedProblem:
         self.local = local
         self.part = part
         self.group = group
-        self.halo = HaloExchange(part, group)
+        # a device TmopProblem on its slab: halo planes packed / unpacked by
+        # library kernels, MINRES device resident (dist_minres_device)
+        self.device_op = hasattr(local, "ctx") and hasattr(local, "lib")
+        self.halo = HaloExchange(part, group, local.ctx if self.device_op else None,
+                                 local.lib if self.device_op else None)
         # boundary-first Hessian action (outer layers + planes first, exchange
         # overlapping the interior, whose E->L runs behind its element slabs
         # on a second stream).  Off by default: at one rank it measures equal
@@ -249,6 +319,8 @@ class DistributedProblem:
 
     def gradient(self, x):
         g = self._from(self.local.gradient(self._to(x)))
+        if self.device_op:
+            return self.halo.sum_planes_device(g, 0)
         return self.halo.sum_planes(g)           # constrained entries: 0 + 0
 
     def hessian_setup(self, x):
@@ -261,13 +333,23 @@ class DistributedProblem:
             y, pending = split(qdata, self._to(v), self.halo.start)
             y = self._from(y)
             self.halo.finish(y, pending)
+        elif self.device_op:
+            y = self.local.hessian_apply(qdata, v)
+            return self.halo.sum_planes_device(y, 1, vfix=v)
         else:
             y = self._from(self.local.hessian_apply(qdata, self._to(v)))
             self.halo.sum_planes(y)
         return self.halo.refix(y, self.fixed2, v)
 
+    def hessian_apply_into(self, qdata, v, out):
+        """Device action into a caller buffer (the MINRES loop)."""
+        self.local.hessian_apply(qdata, v, out=out)
+        return self.halo.sum_planes_device(out, 1, vfix=v)
+
     def hessian_diagonal(self, qdata):
         d = self._from(self.local.hessian_diagonal(qdata))
+        if self.device_op:
+            return self.halo.sum_planes_device(d, 1, cfix=1.0)
         self.halo.sum_planes(d)
         return self.halo.refix(d, self.fixed2, 1.0)
 
@@ -335,6 +417,69 @@ def dist_minres(problem: DistributedProblem, apply_op, b, max_iterations=50, rel
     return x, itn, relres, relres <= rel_tolerance
 
 
+def dist_minres_device(problem: DistributedProblem, qdata, b, max_iterations=50, rel_tolerance=1e-8, inv=None,
+                       check_every=8):
+    """Device-resident MINRES over the slab partition (solvers.py:93-180):
+    per iteration the local action (element kernel + E->L), the halo plane
+    sum + re-fix (pack / NCCL send-recv / unpack), and the library's MINRES
+    phases K1 / K2 / K3 with each inner product reduced over owned entries
+    into a device scalar and all-reduced in-stream -- no host round trip
+    except the state read every `check_every` iterations (a converged state
+    turns later phases into no-ops).  Same recurrence and scalars as the
+    single-GPU fused step.  Returns (x, iterations, rel_residual, converged)."""
+    torch = _torch()
+
+    from . import _lib
+    lp = problem.local
+    lib, ctx = lp.lib, lp.ctx
+    pt = problem.part
+    lp._sync_stream()
+    b = b.reshape(-1).contiguous()
+    n, nn, own = b.numel(), pt.n_local, pt.n_owned
+    x, r1, r2, z, v, w, w1, w2, av = (torch.empty_like(b) for _ in range(9))
+    st = torch.zeros(2 * _lib.MINRES_STATE_BYTES, dtype=torch.uint8, device=b.device)
+    scal = torch.zeros(2, dtype=torch.float64, device=b.device)
+    P = _lib.ptr
+    ip = P(inv) if inv is not None else None
+    _lib.check(lib.tmop_minres_dist_init_a(ctx, n, nn, own, P(b), ip, P(x), P(r1), P(r2), P(z), P(w), P(w2),
+                                           P(scal)), "tmop_minres_dist_init_a")
+    allreduce_(scal[0:1], group=problem.group)
+    _lib.check(lib.tmop_minres_dist_init_b(ctx, n, P(z), P(v), P(scal), P(st)), "tmop_minres_dist_init_b")
+
+    def state(k):
+        from .solvers import _ST
+        return st.cpu().numpy().view(_ST)[k & 1]
+
+    s0 = state(0)
+    if s0["nonpd"]:
+        raise ValueError("preconditioner is not positive definite")
+    if s0["beta1"] == 0.0:
+        return torch.zeros_like(b), 0, 0.0, True
+    k, done = 0, False
+    while k < max_iterations and not done:
+        for _ in range(min(check_every, max_iterations - k)):
+            problem.hessian_apply_into(qdata, v, av)
+            _lib.check(lib.tmop_minres_dist_k1(ctx, n, nn, own, P(av), P(r1), P(v), P(st), k, P(scal)),
+                       "tmop_minres_dist_k1")
+            allreduce_(scal[0:1], group=problem.group)
+            _lib.check(lib.tmop_minres_dist_k2(ctx, n, nn, own, P(av), P(r2), ip, P(z), P(st), k, P(scal)),
+                       "tmop_minres_dist_k2")
+            allreduce_(scal[1:2], group=problem.group)
+            _lib.check(lib.tmop_minres_dist_k3(ctx, n, P(z), P(v), P(w), P(w1), P(w2), P(x), float(rel_tolerance),
+                                               P(st), k, P(scal)), "tmop_minres_dist_k3")
+            r1, r2, av = r2, av, r1
+            w1, w2, w = w2, w, w1
+            k += 1
+        s_ = state(k)
+        if s_["nonpd"]:
+            raise ValueError("preconditioner is not positive definite")
+        if s_["breakdown"]:
+            raise RuntimeError(f"MINRES breakdown at iteration {int(s_['itn'])}")
+        done = bool(s_["done"])
+    s_ = state(k)
+    return x, int(s_["itn"]), float(s_["relres"]), float(s_["relres"]) <= rel_tolerance
+
+
 def dist_newton_solve(problem: DistributedProblem, x0, max_iterations=100, rel_grad_tolerance=1e-10,
                       minres_max=50, minres_rtol=1e-8, preconditioned=True, max_halvings=30,
                       abs_grad_tolerance=1e-12):
@@ -354,8 +499,11 @@ def dist_newton_solve(problem: DistributedProblem, x0, max_iterations=100, rel_g
         if preconditioned:
             d = problem.hessian_diagonal(qd)
             inv = 1.0 / d.abs().clamp_min(1e-12)
-        dx, its, rr, _ = dist_minres(problem, lambda v: problem.hessian_apply(qd, v), g, minres_max,
-                                     minres_rtol, inv)
+        if problem.device_op:
+            dx, its, rr, _ = dist_minres_device(problem, qd, g, minres_max, minres_rtol, inv)
+        else:
+            dx, its, rr, _ = dist_minres(problem, lambda v: problem.hessian_apply(qd, v), g, minres_max,
+                                         minres_rtol, inv)
         alpha, accepted = 1.0, False
         for _ in range(max_halvings + 1):
             xt = x - alpha * dx

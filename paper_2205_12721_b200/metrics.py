@@ -116,12 +116,18 @@ def evaluate(metric, t) -> MetricEval:
 class TargetKind(IntEnum):
     IDEAL_UNIT = 0
     IDEAL_EQUAL_SIZE = 1
+    # EXTENSION (BASELINE configs[4], "size-adaptive targets"; the reference
+    # has constant isotropic W only, metrics.py:282-345): W(x_q) = v_q^(1/d) I
+    # with v_q the nodal target volume field TargetSpec.size interpolated to
+    # the quadrature points (material field: fixed per point while x moves)
+    SIZE_FIELD = 2
 
 
 @dataclass(frozen=True)
 class TargetSpec:
     kind: TargetKind
     h: float | None = None
+    size: object = None     # SIZE_FIELD: nodal target element volume (n_nodes,)
 
 
 @dataclass(frozen=True)
@@ -148,7 +154,8 @@ class TargetData:
 def build_targets(mesh, spec: TargetSpec, rule, volume: float | None = None) -> TargetData:
     """W = I, or W = h I with h = (vol / Ne)^(1/d) from the quadrature volume
     of the mesh (metrics.py:333-345); the volume is integrated on the GPU."""
-    if spec.kind is TargetKind.IDEAL_UNIT:
+    if spec.kind is TargetKind.IDEAL_UNIT or spec.kind is TargetKind.SIZE_FIELD:
+        # SIZE_FIELD: the per-point scales live on the device (tmop_ctx_set_size_field)
         return TargetData(dim=mesh.dim, scale=1.0)
     if spec.h is not None:
         if spec.h <= 0:
@@ -160,3 +167,25 @@ def build_targets(mesh, spec: TargetSpec, rule, volume: float | None = None) -> 
     if volume <= 0:
         raise ValueError(f"mesh volume must be positive, got {volume}")
     return TargetData(dim=mesh.dim, scale=(volume / mesh.n_elements) ** (1.0 / mesh.dim))
+
+
+def size_field(mesh, kind: str = "shell", amplitude: float = 0.5, n_elements: int | None = None):
+    """Synthetic nodal target-volume fields for the size-adaptive runs
+    (BASELINE configs[4]): the uniform element volume 1/Ne of the unit box
+    modulated by 1 + a*f(x) with mean(f) ~ 0, so the total target volume
+    stays near the box volume (the boundary nodes only slide tangentially).
+      shell: f = cos(2 pi r / r0) of the distance to the box centre (a
+             refined spherical shell, the usual adaptivity demo);
+      sine:  f = prod_k sin(2 pi x_k).
+    n_elements: the GLOBAL element count when `mesh` is one slab of a
+    partition (the field is a function of position only)."""
+    x = np.asarray(mesh.coords, dtype=float)
+    base = 1.0 / (n_elements or mesh.n_elements)
+    if kind == "shell":
+        r = np.sqrt(((x - 0.5) ** 2).sum(axis=0))
+        f = np.cos(2.0 * np.pi * r / 0.35)
+    elif kind == "sine":
+        f = np.prod(np.sin(2.0 * np.pi * x), axis=0)
+    else:
+        raise ValueError(f"unknown size field {kind!r}")
+    return base * (1.0 + amplitude * f)

@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib
 from .fe import Basis1D, OpCounter, build_eval_matrices, gauss_legendre_1d, tensor_weights
 from .mesh import Mesh
-from .metrics import (MetricId, TargetData, TargetSpec, build_targets, check_metric_dim,
+from .metrics import (MetricId, TargetData, TargetKind, TargetSpec, build_targets, check_metric_dim,
                       is_template_metric)
 
 __all__ = ["InvalidMeshError", "LimitingConfig", "ObjectiveConfig", "HessQData", "TmopProblem",
@@ -235,13 +235,17 @@ class TmopProblem:
         self.template = is_template_metric(config.metric)
         self.qdata_fields = self.lib.tmop_qdata_fields(ctx)
         self.qdata_stride = int(self.lib.tmop_qdata_stride(ctx))
-        if config.target.kind != 0 and config.target.h is None:
+        if config.target.kind == TargetKind.SIZE_FIELD:
+            self.targets = build_targets(mesh, config.target, self.rule)
+            self._set_size_field(config.target.size)
+        elif config.target.kind != 0 and config.target.h is None:
             vol = self.volume(mesh.coords.ravel())
             self.targets: TargetData = build_targets(mesh, config.target, self.rule, volume=vol)
         else:
             self.targets = build_targets(mesh, config.target, self.rule)
-        _lib.check(self.lib.tmop_ctx_set_target(ctx, self.targets.inv_scale, self.targets.det_w),
-                   "tmop_ctx_set_target")
+        if config.target.kind != TargetKind.SIZE_FIELD:
+            _lib.check(self.lib.tmop_ctx_set_target(ctx, self.targets.inv_scale, self.targets.det_w),
+                       "tmop_ctx_set_target")
         self._lim = None
         if config.limiting is not None:
             # device copies owned here; the context keeps the pointers (operator.py:463-486)
@@ -263,6 +267,27 @@ class TmopProblem:
             nx, ny, nz = (int(c) for c in mesh.element_counts)
             _lib.check(self.lib.tmop_ctx_set_lattice(ctx, nx, ny, nz, _lib.C.byref(acc)), "tmop_ctx_set_lattice")
         self.lattice = bool(acc.value)
+
+    def _set_size_field(self, size):
+        """Size-field targets (TargetKind.SIZE_FIELD, an extension): upload
+        the nodal target volume, compute the per-point 1/s_q on the device."""
+        torch = _torch()
+        if size is None:
+            raise ValueError("TargetKind.SIZE_FIELD needs TargetSpec.size (nodal target volume)")
+        eta = torch.as_tensor(np.ascontiguousarray(size, dtype=np.float64) if not _is_torch(size) else size,
+                              dtype=torch.float64).reshape(-1).to(self.device)
+        if eta.numel() != self.mesh.n_nodes:
+            raise ValueError(f"size field needs {self.mesh.n_nodes} nodal values, got {eta.numel()}")
+        self._size = eta
+        self._sync_stream()
+        _lib.check(self.lib.tmop_ctx_set_size_field(self._ctx, _lib.ptr(eta)), "tmop_ctx_set_size_field")
+        n = self.mesh.n_elements * self.n_quad_total
+        ptr = self.lib.tmop_ctx_point_scale(self._ctx)
+        ts = torch.zeros(n, dtype=torch.float64, device=self.device)
+        _lib.check(self.lib.tmop_axpby(self._ctx, n, 1.0, ptr, 0.0, _lib.ptr(ts)), "tmop_axpby")
+        if not bool(torch.isfinite(ts).all()):
+            raise ValueError("size field: the interpolated target volume is not positive at some quadrature point")
+        self.point_inv_scale = ts
 
     def __del__(self):
         ctx = getattr(self, "_ctx", None)

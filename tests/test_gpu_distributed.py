@@ -30,7 +30,8 @@ def _worker(rank, world, port, results):
 
     import paper_2205_12721_b200 as P
     from oracle import tmop_oracle as O
-    from paper_2205_12721_b200.distributed import DistributedProblem, SlabPartition, dist_minres
+    from paper_2205_12721_b200.distributed import (DistributedProblem, SlabPartition, dist_minres,
+                                                   dist_minres_device, dist_newton_solve)
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -76,6 +77,19 @@ def _worker(rank, world, port, results):
         xd, itd, _, _ = dist_minres(dp, lambda u: dp.hessian_apply(lq, u), dp.gradient(xl), 20, 1e-300, linv)
         out["minres_its"] = (int(mr.iterations), int(itd))
         out["minres_x"] = err(xd, mr.x)
+        # device-resident distributed MINRES: library phases with owned-node
+        # partial dots all-reduced in between, halo pack / unpack kernels
+        assert dp.device_op
+        xdd, itdd, rrd, _ = dist_minres_device(dp, lq, dp.gradient(xl), 20, 1e-300, linv)
+        out["dminres_its"] = int(itdd)
+        out["dminres_x"] = err(xdd, mr.x)
+        out["dminres_vs_eager"] = float((xdd - xd).norm() / xd.norm())
+        # two Newton iterations (device MINRES inside) vs the single-GPU solver
+        xn, recs, ok, msg = dist_newton_solve(dp, xl, max_iterations=2)
+        own = P.newton_solve(x, gp, P.NewtonConfig(max_iterations=2), P.MinresConfig())
+        out["newton_alpha"] = ([r[0] for r in recs], [r.alpha for r in own.trace.records])
+        out["newton_its"] = ([r[3] for r in recs], [r.minres_iterations for r in own.trace.records])
+        out["newton_x"] = err(xn, np.asarray(own.x))
         results[rank] = out
     finally:
         dist.destroy_process_group()
@@ -105,3 +119,47 @@ def test_slab_partition_with_device_operator_matches_global():
         assert out["dot"] <= 1e-14, out
         assert out["minres_its"][0] == out["minres_its"][1] == 20, out
         assert out["minres_x"] <= 1e-10, out
+        assert out["dminres_its"] == 20, out
+        assert out["dminres_x"] <= 1e-10, out
+        assert out["newton_alpha"][0] == out["newton_alpha"][1], out
+        assert out["newton_its"][0] == out["newton_its"][1], out
+        assert out["newton_x"] <= 1e-9, out
+
+
+def test_bench_distributed_schema_gloo_two_ranks_matches_single_rank():
+    """bench.py's multi-GPU leg as the driver launches it (torch.distributed.run,
+    2 ranks) with gloo on the one GPU of the test box, against the 1-rank
+    --force-dist (NCCL) line: same JSON schema, n_gpus = world size."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    common = ["--steps", "3", "--warmup", "3", "--dist-n", "16", "--no-cpu"]
+    one = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "1", "--force-dist"] + common,
+                         capture_output=True, text=True, timeout=900)
+    assert one.returncode == 0, one.stderr[-3000:]
+    two = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dist-backend", "gloo"]
+                         + common, capture_output=True, text=True, timeout=900)
+    assert two.returncode == 0, two.stderr[-3000:]
+    l1 = json.loads([ln for ln in one.stdout.splitlines() if ln.startswith("{")][-1])
+    l2 = json.loads([ln for ln in two.stdout.splitlines() if ln.startswith("{")][-1])
+    assert l1["n_gpus"] == 1 and l2["n_gpus"] == 2
+    assert set(l1) == set(l2)
+    for k in ("headline_leg", "c4_strong", "c4_weak", "newton_iteration", "e2e", "roofline"):
+        assert set(l1[k]) == set(l2[k]), k
+    assert l2["halo_ms_per_step"] > 0 and l2["halo_bytes_per_neighbor"] == 3 * (16 * 2 + 1) ** 2 * 8
+    assert l2["c4_strong"]["global_dofs"] == l1["c4_strong"]["global_dofs"]
+    assert l2["newton_iteration"]["minres_iterations"] == 20
+
+
+def test_bench_gpus_beyond_device_count_fails_loudly():
+    import subprocess
+    import sys
+
+    import torch
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    n = torch.cuda.device_count() + 1
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", str(n), "--steps", "3"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "CUDA device" in r.stderr

@@ -73,7 +73,7 @@ def test_l2e_map_reproduces_add_at_order():
 
 def test_library_exports_every_declared_symbol():
     header = open(os.path.join(ROOT, "include", "tmop_b200.h")).read()
-    declared = set(re.findall(r"^(?:int|int64_t|const char \*)\s*(tmop_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^(?:int|int64_t|const char \*|const double \*)\s*(tmop_\w+)\s*\(", header, re.M))
     assert declared, "no declarations parsed"
     assert declared == set(_lib.EXPORTED)
     lib = _lib.load()            # loads without a GPU; no compute calls here

@@ -223,3 +223,44 @@ def test_cpu_port_matches_reference(name, threads):
     y = CpuApply(p, qd, threads)(g["v"])
     assert rel(y, g["apply"]) <= 1e-12
     assert np.array_equal(y, CpuApply(p, qd, 2)(g["v"]))
+
+
+# ---- size-field targets (extension: parity unpinned -- FD, PA-vs-FA and the
+# constant-field limit, which IS pinned: it equals IDEAL_EQUAL_SIZE) ---------
+
+def _shell_field(mesh, amp=0.5):
+    r = np.sqrt(((mesh.coords - 0.5) ** 2).sum(axis=0))
+    return (1.0 / mesh.n_elements) * (1.0 + amp * np.cos(2.0 * np.pi * r / 0.35))
+
+
+@pytest.mark.parametrize("metric,dim,order", [(O.MU_321, 3, 2), (O.MU_303, 3, 1), (O.MU_302, 3, 2),
+                                              (O.MU_2, 2, 2), (O.MU_7, 2, 3)])
+def test_size_field_operator_consistency(metric, dim, order, rng):
+    mesh = O.box_mesh(dim, (3, 2, 2)[:dim], order)
+    p = O.OracleProblem(mesh, metric, order + 2, target="field", size=_shell_field(mesh))
+    x = O.perturb(mesh, rng, 0.2)
+    v = rng.standard_normal(x.shape)
+    qd = p.hessian_setup(x)
+    assert rel(p.hessian_apply(qd, v), p.fa_matvec(x, v)) <= 1e-12
+    vf = np.where(mesh.fixed.ravel(), 0.0, v)
+    fd = (p.gradient(x + 1e-5 * vf) - p.gradient(x - 1e-5 * vf)) / 2e-5
+    assert rel(p.hessian_apply(qd, vf), fd) <= 1e-5
+    gv = float(p.gradient(x) @ vf)
+    fdf = (p.objective(x + 1e-6 * vf) - p.objective(x - 1e-6 * vf)) / 2e-6
+    assert gv == pytest.approx(fdf, rel=1e-6)
+
+
+def test_size_field_constant_equals_equal_size_target(rng):
+    """eta = h^d everywhere is the reference's IDEAL_EQUAL_SIZE target with
+    that h (metrics.py:333-345) -- the pinned limit of the extension."""
+    mesh = O.box_mesh(3, (3, 2, 2), 2)
+    h = 0.37
+    pf = O.OracleProblem(mesh, O.MU_303, 4, target="field", size=np.full(mesh.n_nodes, h ** 3))
+    pc = O.OracleProblem(mesh, O.MU_303, 4, target="size", h=h)
+    x = O.perturb(mesh, rng, 0.2)
+    v = rng.standard_normal(x.shape)
+    assert pf.objective(x) == pytest.approx(pc.objective(x), rel=1e-13)
+    assert rel(pf.gradient(x), pc.gradient(x)) <= 1e-13
+    qf, qc = pf.hessian_setup(x), pc.hessian_setup(x)
+    assert rel(pf.hessian_apply(qf, v), pc.hessian_apply(qc, v)) <= 1e-13
+    assert rel(pf.hessian_diagonal(qf), pc.hessian_diagonal(qc)) <= 1e-13
