@@ -324,7 +324,7 @@ def c1_solve():
     return out
 
 
-def c5_solve(n=96, max_newton=25):
+def c5_solve(n=96, max_newton=40):
     """BASELINE configs[4] (C5) on one GPU: 3D Q2 hexes, shape+size metric
     mu_321 with size-adaptive targets (TargetKind.SIZE_FIELD: nodal target
     volume 'shell' field, W_q = v_q^(1/3) I), perturbed start, full Newton
@@ -522,10 +522,11 @@ def dist_env():
 def _hash_unit(idx, salt):
     """Counter-based uniform(-1, 1) from global indices (splitmix64): every
     rank draws the same value for a shared node, whatever the partition."""
-    z = (idx.astype(np.uint64) + np.uint64(salt) * np.uint64(0x9E3779B97F4A7C15)) * np.uint64(0xBF58476D1CE4E5B9)
-    z ^= z >> np.uint64(31)
-    z *= np.uint64(0x94D049BB133111EB)
-    z ^= z >> np.uint64(29)
+    with np.errstate(over="ignore"):            # modular uint64 arithmetic
+        z = (idx.astype(np.uint64) + np.uint64(salt) * np.uint64(0x9E3779B97F4A7C15)) * np.uint64(0xBF58476D1CE4E5B9)
+        z ^= z >> np.uint64(31)
+        z *= np.uint64(0x94D049BB133111EB)
+        z ^= z >> np.uint64(29)
     return (z >> np.uint64(11)).astype(np.float64) * (2.0 / 2 ** 53) - 1.0
 
 
@@ -653,10 +654,9 @@ def dist_newton_iteration(dp, prob, x, group=None):
     alpha = 1.0
     for _ in range(31):
         xt = x - alpha * dx
-        if dp.min_det_jacobian(xt) > 0.0 and dp.objective(xt) < 1.2 * f:
-            gt = dp.gradient(xt)
-            if float(np.sqrt(dp.dot(gt, gt))) < 1.2 * ng:
-                break
+        md, ft, gt = dp.evaluate_trial(xt)          # one fused element pass per trial
+        if md > 0.0 and ft < 1.2 * f and float(np.sqrt(dp.dot(gt, gt))) < 1.2 * ng:
+            break
         alpha *= 0.5
     torch.cuda.synchronize()
     t4 = time.perf_counter()
@@ -667,22 +667,56 @@ def dist_newton_iteration(dp, prob, x, group=None):
             "alpha": alpha, "initial_gradient_ms": t[4]}
 
 
+def dist_c5(rank, world, device, n, group=None, iters=5):
+    """BASELINE configs[4] over z-slabs: Q2 mu_321 with size-field targets
+    (the 'shell' target-volume field of the GLOBAL mesh), global n x n x nN
+    hexes, `iters` distributed Newton iterations (device MINRES, cap 50,
+    rtol 1e-8, Jacobi), wall time max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2205_12721_b200 as P
+    from paper_2205_12721_b200.distributed import DistributedProblem, SlabPartition, allreduce_, dist_newton_solve
+    counts = (n, n, n * world)
+    part = SlabPartition(counts, 2, world, rank)
+    mesh = part.local_mesh_direct()
+    eta = P.size_field(mesh, "shell", n_elements=counts[0] * counts[1] * counts[2])
+    prob = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_321, P.TargetSpec(P.TargetKind.SIZE_FIELD, size=eta)),
+                         4, device=device)
+    dp = DistributedProblem(prob, part, mesh.fixed_mask, group=group).to(device)
+    x0 = torch.from_numpy(slab_inputs(part, mesh)[0]).to(device)
+    f0 = dp.objective(x0)
+    dist_newton_solve(dp, x0, max_iterations=1)                 # warm-up (kernel configuration, allocator)
+    torch.cuda.synchronize()
+    dist.barrier(group)
+    t = time.perf_counter()
+    x, recs, ok, msg = dist_newton_solve(dp, x0, max_iterations=iters)
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=device)
+    allreduce_(te, op=dist.ReduceOp.MAX, group=group)
+    te = float(te.cpu()[0])
+    return {"workload": f"C5 over z-slabs: global {n}x{n}x{n * world} Q2 hexes, mu_321, size-field targets (shell), "
+                        f"n_q=4, {iters} Newton iterations", "global_dofs": 3 * (2 * n + 1) ** 2 * (2 * n * world + 1),
+            "solve_s": te, "newton_iterations": len(recs), "minres_iterations": int(sum(r[3] for r in recs)),
+            "ms_per_newton_iteration": 1e3 * te / max(1, len(recs)), "f_initial": f0,
+            "f_final": recs[-1][1] if recs else f0, "message": msg}
+
+
 def nccl_summary():
     """Communicator lines NCCL_DEBUG=INFO wrote to NCCL_DEBUG_FILE (set in
-    main() before the process group starts)."""
+    main() before the process group starts): init, rank count, transports
+    (P2P/NVLS/NET) and channel setup."""
     path = os.environ.get("NCCL_DEBUG_FILE", "")
-    if "%" in path or not path or not os.path.exists(path):
-        import glob
-        cands = sorted(glob.glob(os.path.join("/tmp", f"tmop_nccl.{os.getpid()}.log")))
-        path = cands[0] if cands else ""
+    keys = ("Init COMPLETE", "nRanks", "NVLS", "P2P", "Channel 00", "Connected all", "Using network", "comm 0x",
+            "NCCL version")
     lines = []
     try:
         for ln in open(path):
-            if any(k in ln for k in ("comm 0x", "NVLS", "Channel 00", "Connected all", "Using network", "P2P/")):
-                lines.append(ln.strip()[-160:])
-    except Exception:
-        pass
-    return lines[:24]
+            if any(k in ln for k in keys):
+                lines.append(ln.strip()[-200:])
+    except Exception as err:
+        lines.append(f"(no NCCL log at {path!r}: {err})")
+    return lines[:30]
 
 
 DIST_ORDERS = {"c3_weak": (2, 160, 4), "c4": (3, 112, 5)}   # leg -> (p, elements per axis per slab, n_q)
@@ -705,7 +739,13 @@ def run_distributed(args, rank, world, local, device, metric, config, group=None
     with ClockSampler(local) as cs:
         head, (prob, dp, qd, x) = dist_leg(rank, world, device, (n2, n2, n2 * world), p2, q2, args.steps,
                                            args.warmup, group)
-    newton = None if args.no_newton else dist_newton_iteration(dp, prob, x, group)
+    newton = None
+    if not args.no_newton:
+        # the better of two iterations from the same x (the first configures
+        # kernels and fills the caching allocator), as the 1-GPU line does
+        runs = [dist_newton_iteration(dp, prob, x, group) for _ in range(2)]
+        newton = min(runs, key=lambda r: r["ms"])
+        newton["runs_ms"] = [r["ms"] for r in runs]
     del prob, dp, qd, x
     import gc
     gc.collect()
@@ -715,6 +755,9 @@ def run_distributed(args, rank, world, local, device, metric, config, group=None
     gc.collect()
     torch.cuda.empty_cache()
     weak, _ = dist_leg(rank, world, device, (n3, n3, n3 * world), p3, q3, args.steps, args.warmup, group)
+    gc.collect()
+    torch.cuda.empty_cache()
+    c5 = None if args.no_newton else dist_c5(rank, world, device, args.dist_n or 96, group)
     if rank != 0:
         return
     peak = peaks()[0]
@@ -737,6 +780,7 @@ def run_distributed(args, rank, world, local, device, metric, config, group=None
                     "d2h_bytes_per_step": head["d2h_bytes_per_step"], "ms_per_step": head["e2e_ms_per_step"]},
             "gpu_launches": (2 * OVERLAP_SLABS + 2) * args.steps, "clocks": cs.summary(),
             "headline_leg": head, "c4_strong": strong, "c4_weak": weak, "newton_iteration": newton,
+            "c5_dist": c5,
             "nccl": nccl_summary()}
     print(json.dumps(line))
 

@@ -253,6 +253,47 @@ __device__ __forceinline__ void hess_template(const double (&c)[4], const double
     }
 }
 
+// 3D template block from C = cof(T) (S = itau C) without forming S g^T S:
+// with tau = det T, C g^T C = (C:g) C - tau dcof(T)[g] (differentiate
+// cof(T) = tau T^-T), so
+//   z = c0 g + (w1 + k3 ds) C + w2 T - k3 dcof(T)[g],  k3 = c3 itau,
+// w1 = (c1 T:g + c2 ds) itau, w2 = c1 ds, ds = itau C:g -- 72 FP64 ops for
+// the g-dependent part instead of 90 (two 3x3 products).  dcof(T)[g]_ij is
+// the cyclic 2x2 minor rule of mcof differentiated: 4 products per entry.
+#ifndef TMOP_DCOF
+#define TMOP_DCOF 1
+#endif
+__device__ __forceinline__ void hess_tpl_cof3(const double (&c)[4], const double (&C)[3][3], const double (&T)[3][3],
+                                              double itau, const double (&g)[3][3], double (&z)[3][3]) {
+  double dt = 0.0, cgd = 0.0;
+  {
+    double r[3], q[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      r[i] = T[i][0] * g[i][0] + T[i][1] * g[i][1] + T[i][2] * g[i][2];
+      q[i] = C[i][0] * g[i][0] + C[i][1] * g[i][1] + C[i][2] * g[i][2];
+    }
+    dt = (r[0] + r[1]) + r[2];
+    cgd = (q[0] + q[1]) + q[2];
+  }
+  const double ds = itau * cgd;
+  const double w1 = (c[1] * dt + c[2] * ds) * itau;
+  const double w2 = c[1] * ds;
+  const double k3 = c[3] * itau;
+  const double wc = w1 + k3 * ds;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+      const double dc = (g[i1][j1] * T[i2][j2] + T[i1][j1] * g[i2][j2]) -
+                        (g[i1][j2] * T[i2][j1] + T[i1][j2] * g[i2][j1]);
+      z[i][j] = c[0] * g[i][j] + wc * C[i][j] + w2 * T[i][j] - k3 * dc;
+    }
+  }
+}
+
 // Non-template metrics (mu_302, mu_321): first derivative and Hessian action
 // from T and S = T^{-T}.  With I1 = |T|^2, J = |S|^2, M = S S^T S:
 //   dJ/dT = -2 M,  dS[g] = -S g^T S,  dM[g] = dS S^T S + S dS^T S + S S^T dS.

@@ -632,6 +632,15 @@ __device__ __forceinline__ void lean_load(const double *qd, int QP, double (&T)[
 template <int D, bool NTM>
 __device__ __forceinline__ void lean_hess(int metric, const double *qd, int QP, const double (&g)[D][D],
                                           double (&z)[D][D]) {
+  if constexpr (D == 3 && !NTM && TMOP_DCOF) {
+    double T[3][3], C[3][3], c[4];
+    load_point<3>(qd, QP, T);
+    const double k0 = qd[9 * QP], itau = qd[10 * QP];
+    mcof<3>(T, C);
+    lean_coeffs(metric, k0, itau, mfro2<3>(T), c);
+    hess_tpl_cof3(c, C, T, itau, g, z);
+    return;
+  }
   double T[D][D], S[D][D], k0, itau;
   lean_load<D>(qd, QP, T, S, k0, itau);
   if constexpr (!NTM) {

@@ -191,7 +191,16 @@ __device__ __forceinline__ void xl_point(int metric, const double (&qd)[11], con
 #pragma unroll
     for (int k = 0; k < N; ++k) av[c][n][k] += (n == 0 ? tg[k] : tb[k]) * z;
   };
-  if constexpr (!NTM) {
+  if constexpr (!NTM && TMOP_DCOF) {
+    const double k0 = qd[9], itau = qd[10];
+    double c[4], z[3][3];
+    lean_coeffs(metric, k0, itau, tdot(T, T), c);
+    hess_tpl_cof3(c, C, T, itau, g, z);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int n = 0; n < 3; ++n) acc(a, n, z[a][n]);
+  } else if constexpr (!NTM) {
     const double k0 = qd[9], itau = qd[10];
     double c[4];
     lean_coeffs(metric, k0, itau, tdot(T, T), c);

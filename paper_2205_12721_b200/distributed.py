@@ -326,6 +326,26 @@ class DistributedProblem:
     def hessian_setup(self, x):
         return self.local.hessian_setup(self._to(x))
 
+    def evaluate_trial(self, x):
+        """(min det, F, grad F) of a line-search trial point: the local fused
+        pass (TmopProblem.evaluate_trial) when available, then MIN / SUM
+        all-reduces and the gradient's plane sum; F and grad are None when
+        the mesh is inverted anywhere (solvers.py:210-216)."""
+        import torch.distributed as dist
+        ev = getattr(self.local, "evaluate_trial", None)
+        if ev is None or not self.device_op:
+            md = self.min_det_jacobian(x)
+            if not md > 0.0:
+                return md, None, None
+            return md, self.objective(x), self.gradient(x)
+        md, f, g = ev(self._to(x))
+        md = self._reduce(md, dist.ReduceOp.MIN)
+        if not md > 0.0:
+            return md, None, None
+        # every rank computed F and grad (its local mesh is valid): finish them
+        f = self._reduce(f, dist.ReduceOp.SUM)
+        return md, f, self.halo.sum_planes_device(g, 0)
+
     def hessian_apply(self, qdata, v):
         split = getattr(self.local, "hessian_apply_boundary_first", None)
         if split is not None and self.overlap:

@@ -180,6 +180,31 @@ def kershaw_case(name):
                         restriction=mesh.restriction)
 
 
+def report_case(name):
+    """Reporting formats of the reference driver (bench.py:31-37, 244-330):
+    VTK Lagrange-hex permutations p = 1..4, the VTK text of a small Kershaw
+    mesh, and the CSV row of a RunReport with fixed values."""
+    import tempfile as _tf
+
+    from tmopbench import bench as rb
+    out = {f"perm_p{p}": rb.vtk_lagrange_hex_permutation(p) for p in (1, 2, 3, 4)}
+    mesh = tb.apply_kershaw(tb.build_cartesian(tb.MeshSpec(3, 6, 2, 2, order=2)), 0.3, 0.3)
+    with _tf.TemporaryDirectory() as d:
+        path = os.path.join(d, "m.vtk")
+        rb.write_vtk(mesh, path, title="kershaw initial mesh")
+        out["vtk_text"] = np.array(open(path).read())
+    times = {"total": 12.5, "gradient": 0.1 / 3, "hessian_setup": 1.0 / 7, "hessian_apply": 9.87654321,
+             "linesearch": 2e-5, "objective": 0.01}
+    rep = rb.RunReport(nx=24, ny=24, nz=24, order=1, n_quad=9, epsy=0.3, epsz=0.3, metric=303, preconditioned=True,
+                       dofs_per_component=15625, dofs_total=46875, quad_points=24 ** 3 * 729, newton_iterations=13,
+                       minres_iterations=650, times=times, f_initial=43335.601057054526, f_final=-4.279e-12,
+                       relgrad_final=7.68e-10, min_det_initial=3.78e-06, min_det_final=4.6296296296296e-06,
+                       max_dev_uniform=8.41e-9, status="failed", success=False)
+    out["csv_row"] = np.array(",".join(rep.csv_row()))
+    out["csv_header"] = np.array(",".join(rb.CSV_COLUMNS))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+
+
 def main():
     for p in (1, 2, 3, 4):
         for nq in sorted({p + 1, p + 2}):
@@ -210,4 +235,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--only", "report"]:
+        report_case("report_formats")
+    else:
+        main()

@@ -79,3 +79,28 @@ def test_reference_line_search_and_minres_accept_our_operator(tb, rng):
     assert np.linalg.norm(np.asarray(own.x) - r.x) <= 1e-10 * np.linalg.norm(r.x)
     ls = tb.line_search(g["x"], r.x, prob, f0=prob.objective(g["x"]), grad_norm0=float(np.linalg.norm(b)))
     assert ls.alpha > 0 and ls.min_det > 0
+
+
+def test_kershaw_run_benchmark_on_gpu(tmp_path):
+    """The reference driver flow (bench.py:171-241) through
+    paper_2205_12721_b200.kershaw_bench.run_benchmark on the GPU: CSV row with
+    the reference columns, VTK files, per-kernel buckets, and the trajectory
+    of the pinned small Kershaw case (tests/golden/kershawnewton_6x4x4_p2_q4)."""
+    from paper_2205_12721_b200 import kershaw_bench as KB
+    g = load_golden("kershawnewton_6x4x4_p2_q4")
+    cfg = KB.BenchConfig(nx=6, ny=4, nz=4, order=2, n_quad=4, csv_path=os.path.join(tmp_path, "r.csv"),
+                         vtk_prefix=os.path.join(tmp_path, "m"))
+    rep = KB.run_benchmark(cfg)
+    assert rep.success and rep.status == "ok"
+    assert abs(rep.newton_iterations - len(g["records"])) <= 3
+    assert rep.max_dev_uniform <= 1e-9
+    row = KB.read_csv_row(cfg.csv_path)
+    assert list(row) == list(KB.CSV_COLUMNS) and row["status"] == "ok"
+    assert int(row["newton_iters"]) == rep.newton_iterations
+    assert rep.times["hessian_apply"] > 0 and rep.times["hessian_setup"] > 0 and rep.times["linesearch"] > 0
+    assert sum(rep.times[k] for k in KB.KERNELS) <= rep.times["total"]
+    for s in ("initial", "final"):
+        txt = open(f"{cfg.vtk_prefix}_{s}.vtk").read()
+        assert txt.count("\n72") == 6 * 4 * 4
+    fused = KB.run_benchmark(KB.BenchConfig(nx=6, ny=4, nz=4, order=2, n_quad=4), fused=True)
+    assert fused.newton_iterations == rep.newton_iterations

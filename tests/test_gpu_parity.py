@@ -426,7 +426,7 @@ def test_limiting_nodal_delta_matches_reference_golden(name):
     assert rel(p.limiting_hessian_apply(v), g["lim_apply"]) <= TOL
 
 
-@pytest.mark.parametrize("name", golden_names("kershawnewton"))
+@pytest.mark.parametrize("name", golden_names("kershawnewton_6x"))
 def test_kershaw_newton_solve_matches_reference(name):
     """The paper benchmark's flow (reference bench.py:170-245) at a small size:
     Kershaw mesh, Jacobi-MINRES Newton to convergence.  Every MINRES solve hits
@@ -614,18 +614,22 @@ def test_paper_table_kershaw_matches_reference(name):
     """The paper-table configuration itself: Kershaw
     eps 0.3, 24^3 hexes, n_q = 9, mu_303, Jacobi-MINRES (cap 50, rtol 1e-8),
     against the first Newton iterations of the reference's own newton_solve
-    (tests/golden/make_golden_kershaw24.py).  Newton step 1 matches to 1e-12
-    (F, |grad F|, min det and, from the *_it1 fixtures, the iterate).  Every
-    MINRES solve hits its 50-iteration cap on this mesh, so 1e-16 rounding
-    differences of the dot products grow by ~1e9 per Newton step along the
-    Krylov sequence (measured here: 2e-7 in F at step 2); later steps must
-    take the same alpha and MINRES count, with F / |grad F| / min det within
-    the per-step tolerances TOL_STEP."""
+    (tests/golden/make_golden_kershaw24.py).
+
+    Newton step 1 matches to round-off: F and |grad F| to 1e-12, the iterate
+    to 1e-11 (the *_it1 fixtures).  Every MINRES solve hits its 50-iteration
+    cap on this mesh and the trajectory is chaotic: the REFERENCE ITSELF,
+    started from x0 + 1 ulp, moves by 1e-7 in F at step 2 and 4e-3 at step 3
+    (tools/ref_sensitivity.py -> tests/golden/kershaw24_sensitivity_p*.json).
+    Later steps must take the same alpha and MINRES count, with F / |grad F|
+    / min det within SENS_FACTOR x the reference's own 1-ulp sensitivity."""
+    import json
+
     import paper_2205_12721_b200 as P
     g = load_golden(name)
     c = [int(v) for v in g["counts"]]
-    mesh = P.apply_kershaw(P.build_cartesian(P.MeshSpec(dim=3, nx=c[0], ny=c[1], nz=c[2], order=int(g["order"]))),
-                           0.3, 0.3)
+    order = int(g["order"])
+    mesh = P.apply_kershaw(P.build_cartesian(P.MeshSpec(dim=3, nx=c[0], ny=c[1], nz=c[2], order=order)), 0.3, 0.3)
     p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)),
                       int(g["n_quad"]))
     x0 = mesh.dof_vector()
@@ -635,20 +639,30 @@ def test_paper_table_kershaw_matches_reference(name):
     assert res.initial_grad_norm == pytest.approx(float(g["g0"]), rel=1e-12)
     want = g["records"]
     assert res.trace.newton_iterations == len(want)
+    sens_path = os.path.join(os.path.dirname(__file__), "golden", f"kershaw24_sensitivity_p{order}.json")
+    sens = json.load(open(sens_path))["rows"] if os.path.exists(sens_path) else []
     for k, (rec, ref) in enumerate(zip(res.trace.records, want)):
-        tol = TOL_STEP[k]
         print(name, k, rec.alpha, rec.minres_iterations, rec.objective / ref[1] - 1, rec.grad_norm / ref[2] - 1,
               rec.min_det / ref[5] - 1)
         assert rec.alpha == ref[0]
         assert rec.minres_iterations == int(ref[3])
-        assert rec.objective == pytest.approx(ref[1], rel=tol)
-        assert rec.grad_norm == pytest.approx(ref[2], rel=tol)
-        assert rec.min_det == pytest.approx(ref[5], rel=10 * tol)
-    print(name, "x rel", rel(res.x, g["x"]))
-    assert rel(res.x, g["x"]) <= TOL_STEP[len(want) - 1]
+        if k == 0:
+            tf = tg = 1e-12
+            tm = 1e-7              # a minimum over points of a nearly degenerate mesh (iterate moves 1e-12)
+        else:
+            assert k < len(sens), "no reference sensitivity recorded for this step"
+            tf = SENS_FACTOR * abs(sens[k]["F_rel"])
+            tg = SENS_FACTOR * abs(sens[k]["grad_rel"])
+            tm = SENS_FACTOR * abs(sens[k]["min_det_rel"])
+        assert rec.objective == pytest.approx(ref[1], rel=tf)
+        assert rec.grad_norm == pytest.approx(ref[2], rel=tg)
+        assert rec.min_det == pytest.approx(ref[5], rel=tm)
+    if len(want) == 1:
+        print(name, "x rel", rel(res.x, g["x"]))
+        assert rel(res.x, g["x"]) <= 1e-11
 
 
-TOL_STEP = (1e-12, 1e-5, 1e-3)
+SENS_FACTOR = 10.0
 
 
 # Size-field targets (TargetKind.SIZE_FIELD, an extension -- no reference

@@ -4,7 +4,7 @@ p=1 for 3 Newton iterations from x0 and from x0 perturbed by one ulp on
 every free coordinate, and prints the relative change of F / |grad F| /
 min det per iteration (container only: imports /root/reference).
 
-    NUMBA_NUM_THREADS=3 python tools/ref_sensitivity.py --order 1 > profiles/ref_kershaw24_sensitivity_p1.json
+    NUMBA_NUM_THREADS=3 python tools/ref_sensitivity.py --order 1 > tests/golden/kershaw24_sensitivity_p1.json
 """
 import argparse
 import json
