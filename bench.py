@@ -34,6 +34,10 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL communicator logging for the multi-GPU legs (read back by nccl_summary);
+# set before torch loads NCCL.  %p = pid.
+os.environ.setdefault("NCCL_DEBUG", "INFO")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/tmop_nccl.%p.log")
 
 SEED = 20240901
 ORDERS = {1: (200, 3), 2: (160, 4), 3: (107, 5), 4: (80, 6)}   # p -> (elements per axis, n_q)
@@ -324,7 +328,7 @@ def c1_solve():
     return out
 
 
-def c5_solve(n=96, max_newton=40):
+def c5_solve(n=96, max_newton=60):
     """BASELINE configs[4] (C5) on one GPU: 3D Q2 hexes, shape+size metric
     mu_321 with size-adaptive targets (TargetKind.SIZE_FIELD: nodal target
     volume 'shell' field, W_q = v_q^(1/3) I), perturbed start, full Newton
@@ -706,7 +710,7 @@ def nccl_summary():
     """Communicator lines NCCL_DEBUG=INFO wrote to NCCL_DEBUG_FILE (set in
     main() before the process group starts): init, rank count, transports
     (P2P/NVLS/NET) and channel setup."""
-    path = os.environ.get("NCCL_DEBUG_FILE", "")
+    path = os.environ.get("NCCL_DEBUG_FILE", "").replace("%p", str(os.getpid()))
     keys = ("Init COMPLETE", "nRanks", "NVLS", "P2P", "Channel 00", "Connected all", "Using network", "comm 0x",
             "NCCL version")
     lines = []
@@ -899,8 +903,6 @@ def main():
                 port = sk.getsockname()[1]
             os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
                               MASTER_PORT=str(port))
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/tmop_nccl.{os.getpid()}.log")
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:

@@ -44,6 +44,7 @@ def solve(order, n, nq, precond=True):
             "newton_iterations": tr.newton_iterations if tr else None,
             "minres_iterations": tr.minres_total if tr else None,
             "status": status, "message": msg, "f_initial": f0, "f_final": prob.objective(x),
+            "f_per_iteration": [float(f"{r.objective:.6g}") for r in tr.records] if tr else None,
             "max_dev_uniform": float(np.max(np.abs(xf - uniform)))}
 
 
