@@ -36,8 +36,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 # NCCL communicator logging for the multi-GPU legs (read back by nccl_summary);
 # set before torch loads NCCL.  %p = pid.
-os.environ.setdefault("NCCL_DEBUG", "INFO")
-os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/tmop_nccl.%p.log")
+if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+    os.environ["NCCL_DEBUG"] = "INFO"
+os.environ["NCCL_DEBUG_FILE"] = "/tmp/tmop_nccl.%p.log"
 
 SEED = 20240901
 ORDERS = {1: (200, 3), 2: (160, 4), 3: (107, 5), 4: (80, 6)}   # p -> (elements per axis, n_q)
@@ -594,17 +595,17 @@ def dist_leg(rank, world, device, counts, order, nq, steps, warmup, group=None, 
     total, halo, loc = (float(u) for u in t.cpu())
     nx, ny, nz = counts
     global_dofs = 3 * (nx * order + 1) * (ny * order + 1) * (nz * order + 1)
-    # e2e through the distributed public API: pinned host v -> device ->
-    # DistributedProblem.hessian_apply -> pinned host y, every step
+    # e2e through the distributed public API: pinned host v -> pinned host y
+    # every step (DistributedProblem.hessian_apply_host: the slab-pipelined
+    # H2D / action / D2H, then the plane sums on the device)
     vpin = v.cpu().pin_memory()
     ypin = torch.empty_like(vpin).pin_memory()
+    dp.hessian_apply_host(qd, vpin, ypin)          # (configures the pipeline streams)
     dist.barrier(group)
     torch.cuda.synchronize()
     te0 = time.perf_counter()
     for _ in range(steps):
-        vd = vpin.to(device, non_blocking=True)
-        yd = dp.hessian_apply(qd, vd)
-        ypin.copy_(yd, non_blocking=True)
+        dp.hessian_apply_host(qd, vpin, ypin)
         torch.cuda.synchronize()
     te = torch.tensor([time.perf_counter() - te0], dtype=torch.float64, device=device)
     allreduce_(te, op=dist.ReduceOp.MAX, group=group)

@@ -10,6 +10,7 @@
 
 #include "tmop_lim.cuh"
 #include "tmop_xl.cuh"
+#include "tmop_xld.cuh"
 #include "tmop_diag.cuh"
 #include "tmop_elem.cuh"
 #include "tmop_internal.h"
@@ -65,8 +66,44 @@ int launch_xl(ElemArgs &a, const Tab &t, cudaStream_t s) {
   return grid;
 }
 
+// TMOP_XLD=0 keeps the work-item diagonal (diag2_kernel) everywhere.
+inline bool xld_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = std::getenv("TMOP_XLD");
+    v = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// 3D p <= 3 diagonal in x-line form (tmop_xld.cuh): one persistent wave.
+template <int N, int Q, bool NTM>
+int launch_xld(ElemArgs &a, const Tab &t, cudaStream_t s) {
+  using XC = XldCfg<N, Q>;
+  a.ngroups = (a.ne + XC::EPB - 1) / XC::EPB;
+  a.e_es = XC::EPB == 16 ? 4 : XC::EPB == 8 ? 3 : 2;
+  auto kfn = xld_kernel<N, Q, NTM>;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, XC::SMEM) != cudaSuccess) return -2;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, XC::NT, XC::SMEM) != cudaSuccess || nb < 1) nb = 1;
+    per_sm = nb;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>(std::min<int64_t>(a.ngroups, (int64_t)sms * per_sm), GRID_CAP);
+  if (grid == 0) return 0;
+  kfn<<<grid, XC::NT, XC::SMEM, s>>>(a, t);
+  return grid;
+}
+
 template <int DIM, int N, int Q, bool NTM>
 int launch_diag(ElemArgs &a, const Tab &t, cudaStream_t s) {
+  if constexpr (DIM == 3 && xld_supported<N, Q>()) {
+    if (xld_enabled()) return launch_xld<N, Q, NTM>(a, t, s);
+  }
   using DC = DiagCfg<DIM, N, Q>;
   a.ngroups = (a.ne + DC::EPB - 1) / DC::EPB;
   const int grid = (int)std::min<int64_t>(a.ngroups, GRID_CAP);

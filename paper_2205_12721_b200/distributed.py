@@ -361,6 +361,46 @@ class DistributedProblem:
             self.halo.sum_planes(y)
         return self.halo.refix(y, self.fixed2, v)
 
+    def hessian_apply_host(self, qdata, vh, out=None):
+        """Host-resident action (pinned torch CPU v -> pinned y): the local
+        slab runs the pipelined host path (H2D / element kernel + E->L / D2H
+        overlapped per z-slab, TmopProblem._apply_host_pipelined), then only
+        the two shared planes (3 x plane values each) go back to the device for
+        the halo sum and the constraint re-fix, and return to host."""
+        torch = _torch()
+        y = self.local.hessian_apply(qdata, vh, out=out)
+        pt = self.part
+        if not (pt.has_lower or pt.has_upper):
+            return y
+        pl, nn = pt.plane, pt.n_local
+        dev = self.fixed2.device
+        y2, v2 = y.view(3, nn), vh.view(3, nn)
+        sides = ([slice(0, pl)] if pt.has_lower else []) + ([slice(nn - pl, nn)] if pt.has_upper else [])
+        yp = torch.cat([y2[:, sl] for sl in sides], 1).to(dev, non_blocking=True)
+        vp = torch.cat([v2[:, sl] for sl in sides], 1).to(dev, non_blocking=True)
+        fp = torch.cat([self.fixed2[:, sl] for sl in sides], 1)
+        # exchange the local partial sums of the planes (same protocol as HaloExchange.start)
+        import torch.distributed as dist
+        ops, recv, k = [], [], 0
+        for side, nb in (("lo", pt.rank - 1), ("hi", pt.rank + 1)):
+            if (side == "lo" and not pt.has_lower) or (side == "hi" and not pt.has_upper):
+                continue
+            snd, _ = _staged(yp[:, k * pl:(k + 1) * pl].contiguous(), self.group)
+            rcv = torch.empty_like(snd)
+            ops += [dist.P2POp(dist.isend, snd, nb, self.group), dist.P2POp(dist.irecv, rcv, nb, self.group)]
+            recv.append((k, rcv))
+            k += 1
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        for k, rcv in recv:
+            yp[:, k * pl:(k + 1) * pl] += rcv.to(dev)
+        yp = torch.where(fp, vp, yp).cpu()
+        k = 0
+        for sl in sides:
+            y2[:, sl] = yp[:, k * pl:(k + 1) * pl]
+            k += 1
+        return y
+
     def hessian_apply_into(self, qdata, v, out):
         """Device action into a caller buffer (the MINRES loop)."""
         self.local.hessian_apply(qdata, v, out=out)

@@ -62,6 +62,9 @@ def _worker(rank, world, port, results):
         dp.overlap = True                        # boundary layers first, exchange overlapping the interior
         out["overlap_bitwise"] = bool(torch.equal(ya, dp.hessian_apply(lq, vl)))
         dp.overlap = False
+        # host-resident pipelined action + device plane sums == the device path
+        vpin = vl.cpu().pin_memory()
+        out["host_bitwise"] = bool(torch.equal(dp.hessian_apply_host(lq, vpin), ya.cpu()))
         out["grad"] = err(dp.gradient(xl), gp.gradient(x))
         out["diag"] = err(dp.hessian_diagonal(lq), gp.hessian_diagonal(gq))
         out["obj"] = abs(dp.objective(xl) - gp.objective(x)) / abs(gp.objective(x))
@@ -90,6 +93,17 @@ def _worker(rank, world, port, results):
         out["newton_alpha"] = ([r[0] for r in recs], [r.alpha for r in own.trace.records])
         out["newton_its"] = ([r[3] for r in recs], [r.minres_iterations for r in own.trace.records])
         out["newton_x"] = err(xn, np.asarray(own.x))
+        # size-field targets (mu_321) over the partition vs the global operator
+        eta = P.size_field(gmesh, "shell")
+        cfw = P.ObjectiveConfig(P.MetricId.MU_321, P.TargetSpec(P.TargetKind.SIZE_FIELD, size=eta))
+        gw = P.TmopProblem(gmesh, cfw, NQ)
+        lw = P.TmopProblem(lmesh, P.ObjectiveConfig(P.MetricId.MU_321, P.TargetSpec(
+            P.TargetKind.SIZE_FIELD, size=eta[part.node_lo:part.node_hi])), NQ)
+        dw = DistributedProblem(lw, part, lmesh.fixed_mask).to("cuda")
+        gqw, lqw = gw.hessian_setup(x), dw.hessian_setup(xl)
+        out["size_apply"] = err(dw.hessian_apply(lqw, vl), gw.hessian_apply(gqw, v))
+        out["size_grad"] = err(dw.gradient(xl), gw.gradient(x))
+        out["size_obj"] = abs(dw.objective(xl) - gw.objective(x)) / abs(gw.objective(x))
         results[rank] = out
     finally:
         dist.destroy_process_group()
@@ -112,6 +126,7 @@ def test_slab_partition_with_device_operator_matches_global():
         assert out["lattice"], out
         assert out["apply"] <= 1e-13, out
         assert out["overlap_bitwise"], out
+        assert out["host_bitwise"], out
         assert out["grad"] <= 1e-13, out
         assert out["diag"] <= 1e-13, out
         assert out["obj"] <= 1e-13, out
@@ -124,6 +139,7 @@ def test_slab_partition_with_device_operator_matches_global():
         assert out["newton_alpha"][0] == out["newton_alpha"][1], out
         assert out["newton_its"][0] == out["newton_its"][1], out
         assert out["newton_x"] <= 1e-9, out
+        assert out["size_apply"] <= 1e-13 and out["size_grad"] <= 1e-13 and out["size_obj"] <= 1e-13, out
 
 
 def test_bench_distributed_schema_gloo_two_ranks_matches_single_rank():
