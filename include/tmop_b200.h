@@ -166,6 +166,17 @@ int tmop_hessian_apply_elements_range(tmop_ctx *ctx, const double *qdata, const 
 int tmop_hessian_apply_gather_range(tmop_ctx *ctx, const double *v, double *y, int64_t n_begin, int64_t n_end);
 /* AssembleGradDiagonalPA: hessian_diagonal (operator.py:420-459). */
 int tmop_hessian_diagonal(tmop_ctx *ctx, const double *qdata, double *diag);
+/* hessian_setup followed by hessian_diagonal (operator.py:350-371,
+ * 420-459) -- what newton_solve does once per iteration when the Jacobi
+ * preconditioner is on (solvers.py:292-295).  By default the two passes;
+ * with TMOP_SETUP_DIAG_FUSED=1 (3D p <= 3, template metrics, no limiting
+ * term) ONE element pass that forms the diagonal's H-pair values from each
+ * group's records while they are still in shared memory (records written
+ * once, never re-read) -- bitwise the same outputs, measured slower (see
+ * DESIGN.md section 3).  diag is garbage when det_out reports an inverted
+ * element, like the setup's Q-data. */
+int tmop_hessian_setup_diagonal(tmop_ctx *ctx, const double *x, double *qdata, double *diag,
+                                tmop_det_status *det_out);
 /* AddMultPA: gradient (operator.py:328-346). */
 int tmop_gradient(tmop_ctx *ctx, const double *x, double *grad,
                   tmop_det_status *det_out);

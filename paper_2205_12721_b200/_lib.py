@@ -60,6 +60,7 @@ _SIGS = {
     "tmop_limiting_gradient": [_P, _P, _P],
     "tmop_limiting_apply": [_P, _P, _P],
     "tmop_hessian_setup": [_P, _P, _P, _P],
+    "tmop_hessian_setup_diagonal": [_P, _P, _P, _P, _P],
     "tmop_hessian_apply": [_P, _P, _P, _P],
     "tmop_hessian_apply_elements": [_P, _P, _P],
     "tmop_hessian_apply_gather": [_P, _P, _P],

@@ -452,6 +452,36 @@ int tmop_limiting_apply(tmop_ctx *c, const double *v, double *y) {
   return TMOP_OK;
 }
 
+int tmop_hessian_setup_diagonal(tmop_ctx *c, const double *x, double *qdata, double *diag,
+                                tmop_det_status *det_out) {
+  if (!c || !x || !qdata || !diag || !det_out) return fail(TMOP_ERR_ARG, "NULL argument");
+  // The one-pass kernel (xl_kernel<K_SETUP_DIAG>) is opt-in: measured slower
+  // than the two passes (setup 4.3 ms + x-line diagonal 7.6 ms at C3 p = 2:
+  // 11.9 vs 12.5 ms fused; p = 1: 8.8 vs 11.4; p = 3: 10.1 vs 18.0) -- the
+  // fused CTA carries the setup's and the diagonal's shared-memory buffers
+  // and registers at once (255 registers, 2 CTAs / SM at p = 2, 1 at p = 3)
+  // and waits for each group's record store before reusing the buffer.
+  static const bool fused_on = getenv("TMOP_SETUP_DIAG_FUSED") && atoi(getenv("TMOP_SETUP_DIAG_FUSED")) != 0;
+  if (fused_on && metric_is_template(c->metric) && !c->lim_on) {
+    ElemArgs a = base_args(c);
+    a.in = x;
+    a.qout = qdata;
+    const int g = launch_elem(c->dim, c->n1, c->nq, K_SETUP_DIAG, a, c->tab, c->stream);
+    if (g >= 0) {   // fused kernel available (3D p <= 3)
+      CUDA_TRY(cudaGetLastError());
+      c->e_es = a.e_es;
+      launch_fin(g, nullptr, c->part_min, c->part_arg, 0.0, nullptr, 0.0, nullptr, det_out, c->stream);
+      CUDA_TRY(cudaGetLastError());
+      launch_e2l(c->dim, c->nn, e2l_map(c), c->E, c->fixed, 2, nullptr, nullptr, diag, c->stream);
+      CUDA_TRY(cudaGetLastError());
+      return TMOP_OK;
+    }
+  }
+  int rc = tmop_hessian_setup(c, x, qdata, det_out);   // the two separate passes
+  if (rc) return rc;
+  return tmop_hessian_diagonal(c, qdata, diag);
+}
+
 int tmop_hessian_setup(tmop_ctx *c, const double *x, double *qdata, tmop_det_status *det_out) {
   if (!c || !x || !qdata || !det_out) return fail(TMOP_ERR_ARG, "NULL argument");
   ElemArgs a = base_args(c);

@@ -42,7 +42,8 @@ enum Kind : int {
   K_LIM_FIELD = 11,  // limiting gradient / Hessian action (operator.py:497-533)
   K_LIM_DIAG = 12,   // limiting part of hessian_diagonal (operator.py:452-457)
   K_TSCALE = 13,     // size-field targets: per-point 1/scale from a nodal target volume (extension)
-  K_COUNT = 14
+  K_SETUP_DIAG = 14, // hessian_setup + hessian_diagonal from one element pass (3D p <= 3, template metrics)
+  K_COUNT = 15
 };
 
 // Tuning knobs (compile-time overrides for tools/build_variant.sh; 0 = the

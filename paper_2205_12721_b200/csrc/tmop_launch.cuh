@@ -34,6 +34,7 @@ inline bool xl_enabled() {
 // the work-item kernel is faster there.
 template <int N, int KIND>
 constexpr bool xl_kind() {
+  if constexpr (KIND == K_SETUP_DIAG) return N <= 4;
   if constexpr (N >= 5) return KIND == K_ENERGY || KIND == K_MINDET;
   return KIND == K_APPLY || KIND == K_APPLY_NT || KIND == K_GRAD || KIND == K_SETUP || KIND == K_ENERGY ||
          KIND == K_MINDET;
@@ -48,7 +49,7 @@ int launch_xl(ElemArgs &a, const Tab &t, cudaStream_t s) {
   constexpr int smem = XC::template smem<KIND>();
   a.ngroups = (a.ne + XC::EPB - 1) / XC::EPB;
   static_assert(XC::EPB == 16 || XC::EPB == 8 || XC::EPB == 4, "e_es assumes 4-, 8- or 16-element groups");
-  if constexpr (xl_backward<KIND>()) a.e_es = XC::EPB == 16 ? 4 : XC::EPB == 8 ? 3 : 2;
+  if constexpr (xl_backward<KIND>() || KIND == K_SETUP_DIAG) a.e_es = XC::EPB == 16 ? 4 : XC::EPB == 8 ? 3 : 2;
   auto kfn = xl_kernel<N, Q, KIND>;
   static int per_sm = 0;
   if (per_sm == 0) {
@@ -143,6 +144,14 @@ int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
   } else if constexpr (KIND == K_DIAG || KIND == K_DIAG_NT) {
     return launch_diag<DIM, N, Q, KIND == K_DIAG_NT>(a, t, s);
   } else {
+    if constexpr (KIND == K_SETUP_DIAG) {
+      // fused setup + diagonal: 3D x-line only (callers fall back to the two
+      // separate passes on -1)
+      if constexpr (DIM == 3 && xl_kind<N, KIND>() && XlCfg<N, Q>::template smem<KIND>() <= 227 * 1024) {
+        if (xl_enabled() && xld_enabled()) return launch_xl<N, Q, KIND>(a, t, s);
+      }
+      return -1;
+    } else {
     if constexpr (DIM == 3 && xl_kind<N, KIND>() && xl_supported<N, Q>()) {
       if (xl_enabled()) return launch_xl<N, Q, KIND>(a, t, s);
     }
@@ -158,6 +167,7 @@ int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
     }
     kfn<<<grid, CF::NT, smem, s>>>(a, t);
     return grid;
+    }
   }
 }
 
@@ -178,6 +188,7 @@ int launch_kind(int kind, ElemArgs &a, const Tab &t, cudaStream_t s) {
     case K_LIM_FIELD: return launch_one<DIM, N, Q, K_LIM_FIELD>(a, t, s);
     case K_LIM_DIAG: return launch_one<DIM, N, Q, K_LIM_DIAG>(a, t, s);
     case K_TSCALE: return launch_one<DIM, N, Q, K_TSCALE>(a, t, s);
+    case K_SETUP_DIAG: return launch_one<DIM, N, Q, K_SETUP_DIAG>(a, t, s);
     default: return -1;
   }
 }

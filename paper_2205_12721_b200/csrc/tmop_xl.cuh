@@ -41,6 +41,7 @@
 #pragma once
 
 #include "tmop_elem.cuh"
+#include "tmop_xld_parts.cuh"
 
 namespace tmop {
 
@@ -113,9 +114,14 @@ struct XlCfg {
   // written back by one TMA bulk store
   static constexpr int QOFF_S = (BOFF_F + (NP * EPB + 7) / 8 + 1) & ~1;
   static constexpr int SMEM_S = (QOFF_S + EPB * QS) * 8;
+  // setup + diagonal: the diagonal's x^T output A overlays the group's
+  // records once they are stored (XldCfg::R1), its y^T output Bv follows
+  static constexpr int SMEM_SD = (QOFF_S + XldCfg<N, Q>::R1P + XldCfg<N, Q>::BV_SZ * EPB) * 8;
   template <int KIND>
   static constexpr int smem() {
-    return xl_qdata<KIND>() ? SMEM : (xl_backward<KIND>() ? QOFF * 8 : (KIND == K_SETUP ? SMEM_S : SMEM_F));
+    return xl_qdata<KIND>() ? SMEM
+           : (xl_backward<KIND>() ? QOFF * 8
+                                  : (KIND == K_SETUP ? SMEM_S : (KIND == K_SETUP_DIAG ? SMEM_SD : SMEM_F)));
   }
   static constexpr int GJ = (EPB * NP + NT - 1) / NT;      // gather (element, node) pairs per thread
   // CTAs / SM: the backward kinds keep ~110 doubles live in the x-line
@@ -124,6 +130,7 @@ struct XlCfg {
   template <int KIND>
   static constexpr int minb() {
     return TMOP_XL_MINB ? TMOP_XL_MINB
+           : KIND == K_SETUP_DIAG ? XldCfg<N, Q>::MINB
            : (KIND == K_APPLY_NT && TMOP_XL_NT_MINB) ? TMOP_XL_NT_MINB
            // p = 1, n_q = 3 action (144-thread CTAs): 3 CTAs / SM at a 128-register cap (small spill)
            // beat 2 CTAs at 166 registers: overlapped apply 6.46 -> 6.12 ms
@@ -334,7 +341,8 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
   constexpr bool MASK = APPLY;          // the apply zeroes constrained inputs (operator.py:409)
   constexpr bool NTM = KIND == K_APPLY_NT;
   constexpr bool RSUM = KIND == K_ENERGY || KIND == K_VOLUME || KIND == K_GRAD;
-  constexpr bool RMIN = KIND == K_SETUP || KIND == K_GRAD || KIND == K_ENERGY || KIND == K_MINDET;
+  constexpr bool SD = KIND == K_SETUP_DIAG;
+  constexpr bool RMIN = KIND == K_SETUP || SD || KIND == K_GRAD || KIND == K_ENERGY || KIND == K_MINDET;
   constexpr int EPB = XC::EPB, NP = XC::NP, QP = XC::QP, QS = XC::QS, NT = XC::NT;
   constexpr int U_QZ = XC::U_QZ, W_QY = XC::W_QY, W_QZ = XC::W_QZ;
   constexpr int XOFF = BACK ? XC::XOFF : XC::XOFF_F;
@@ -343,7 +351,7 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
   extern __shared__ __align__(16) double smem[];
   double *U = smem;                       // U / Bv
   double *W = smem + XC::U_SZ * EPB;      // A (backward kinds)
-  double *QB = smem + (KIND == K_SETUP ? XC::QOFF_S : XC::QOFF);   // the group's lean Q-data (TMA-staged)
+  double *QB = smem + ((KIND == K_SETUP || SD) ? XC::QOFF_S : XC::QOFF);   // the group's lean Q-data (TMA-staged)
   __shared__ __align__(8) uint64_t qbar;
   __shared__ double red_v[(RSUM || RMIN) ? NT : 1];
   __shared__ int64_t red_i[RMIN ? NT : 1];
@@ -533,7 +541,7 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
           qload(qx, qd);
           xl_point<N, NTM>(a.metric, qd, g, tg, tb, av);
         } else {
-          xl_point_x<KIND, N, Q>(a, t, eg, line, qx, g, tg, tb, av, acc, mn, QS_rec);
+          xl_point_x<SD ? K_SETUP : KIND, N, Q>(a, t, eg, line, qx, g, tg, tb, av, acc, mn, QS_rec);
         }
       }
       if constexpr (BACK) {
@@ -601,7 +609,7 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
         }
       }
     }
-    if constexpr (KIND == K_SETUP) {
+    if constexpr (KIND == K_SETUP || SD) {
       // the group's records are complete in QB: one TMA bulk store
       fence_proxy_async();
       __syncthreads();
@@ -611,10 +619,23 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
         bulk_store(a.qout + e0 * QS, QB, (uint32_t)(cnt * QS * 8));
       }
     }
+    if constexpr (SD) {
+      // the diagonal (operator.py:420-459) from the records still in shared
+      // memory (tmop_xld_parts.cuh): no re-read of the record from HBM
+      double dacc[3][6][N];
+      xld_line<N, Q, false>(a.metric, QB + e * QS + line, t, dacc);
+      if (tid == 0) bulk_wait_read();   // the store has read QB ...
+      __syncthreads();                  // ... and so has every thread: A may overlay it
+      xld_store_a<N, Q>(QB, line, e, dacc);
+      __syncthreads();
+      if (item < Q * N) xld_y<N, Q>(QB, QB + XldCfg<N, Q>::R1P, item, e, t);
+      __syncthreads();
+      if (item < N * N) xld_z<N, Q>(QB + XldCfg<N, Q>::R1P, a.E, grp, item, e, t);
+    }
     // (no end-of-group barrier: the top-of-loop barrier orders this group's
     // reads of U / Bv before the next F1 writes U)
   }
-  if constexpr (KIND == K_SETUP) {
+  if constexpr (KIND == K_SETUP || SD) {
     if (tid == 0) bulk_wait_all();
   }
 

@@ -446,6 +446,24 @@ class TmopProblem:
         return HessQData(data=qd, dim=self.mesh.dim, n_quad_total=self.n_quad_total, template=self.template,
                          host=host, _expand=self._expand_qdata)
 
+    def hessian_setup_diagonal(self, x):
+        """hessian_setup(x) and hessian_diagonal of the result from one element
+        pass (tmop_hessian_setup_diagonal; 3D p <= 3, template metrics);
+        returns (qdata, diagonal).  newton_solve uses it when the Jacobi
+        preconditioner is on (solvers.py:292-295)."""
+        torch = _torch()
+        xt, host = self._in(x)
+        qd = torch.empty((self.mesh.n_elements, self.qdata_stride), dtype=torch.float64, device=self.device)
+        d = torch.empty_like(xt)
+        _lib.check(self.lib.tmop_hessian_setup_diagonal(self._ctx, _lib.ptr(xt), _lib.ptr(qd), _lib.ptr(d),
+                                                        _lib.ptr(self._status)), "tmop_hessian_setup_diagonal")
+        self._count("setup")
+        md, _ = self._det()
+        self._raise_if_inverted(xt, md)
+        qdata = HessQData(data=qd, dim=self.mesh.dim, n_quad_total=self.n_quad_total, template=self.template,
+                          host=host, _expand=self._expand_qdata)
+        return qdata, self._out(d, host)
+
     def _expand_qdata(self, data):
         torch = _torch()
         nf = self.lib.tmop_qdata_reference_fields(self._ctx)

@@ -474,10 +474,16 @@ def newton_solve(x0, problem: ProblemLike, newton_cfg: NewtonConfig | None = Non
     qdata = None
     for _ in range(newton_cfg.max_iterations):
         qdata = None
-        qdata = problem.hessian_setup(x)
         precond = None
-        if minres_cfg.preconditioned:
-            precond = jacobi_preconditioner(problem.hessian_diagonal(qdata), ctx)
+        setup_diag = getattr(problem, "hessian_setup_diagonal", None)
+        if minres_cfg.preconditioned and setup_diag is not None:
+            # setup + diagonal from one element pass (records never re-read)
+            qdata, diag = setup_diag(x)
+            precond = jacobi_preconditioner(diag, ctx)
+        else:
+            qdata = problem.hessian_setup(x)
+            if minres_cfg.preconditioned:
+                precond = jacobi_preconditioner(problem.hessian_diagonal(qdata), ctx)
         fused = (problem, qdata) if getattr(problem, "supports_fused_minres", False) else None
         try:
             mr = minres(lambda v: problem.hessian_apply(qdata, v), g, minres_cfg, precond, ctx, operator=fused)
