@@ -147,7 +147,11 @@ int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
     if constexpr (KIND == K_SETUP_DIAG) {
       // fused setup + diagonal: 3D x-line only (callers fall back to the two
       // separate passes on -1)
-      if constexpr (DIM == 3 && xl_kind<N, KIND>() && XlCfg<N, Q>::template smem<KIND>() <= 227 * 1024) {
+      // (the fused kind lays the diagonal out with the action's group size
+      // and the records-overlay layout: tuning variants that change either
+      // keep the two passes)
+      if constexpr (DIM == 3 && xl_kind<N, KIND>() && XlCfg<N, Q>::template smem<KIND>() <= 227 * 1024 &&
+                    XldCfg<N, Q>::EPB == XlCfg<N, Q>::EPB && XldCfg<N, Q>::OVL) {
         if (xl_enabled() && xld_enabled()) return launch_xl<N, Q, KIND>(a, t, s);
       }
       return -1;

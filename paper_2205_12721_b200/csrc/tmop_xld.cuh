@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(XldCfg<N, Q>::NT, XldCfg<N, Q>::MINB)
   constexpr int EPB = XC::EPB, QS = XC::QS;
   extern __shared__ __align__(16) double smem[];
   double *QB = smem;                           // staged records ...
-  double *A = smem;                            // ... overlaid by the x^T output
+  double *A = smem + XC::AOFF;                 // ... overlaid by the x^T output (OVL) or beside them
   double *Bv = smem + XC::R1P;
   __shared__ __align__(8) uint64_t qbar;
 
@@ -70,11 +70,16 @@ __global__ void __launch_bounds__(XldCfg<N, Q>::NT, XldCfg<N, Q>::MINB)
     double acc[3][6][N];
     xld_line<N, Q, NTM>(a.metric, QB + e * QS + item, t, acc);
     __syncthreads();                           // every record read: A may overwrite QB
+    if constexpr (!XC::OVL) {                  // records consumed: stream in the next group's
+      if (tid == 0 && grp + gridDim.x < a.ngroups) issue(grp + gridDim.x);
+    }
     xld_store_a<N, Q>(A, item, e, acc);
     __syncthreads();
     if (item < Q * N) xld_y<N, Q>(A, Bv, item, e, t);
     __syncthreads();                           // A (= QB) consumed: stream in the next group's records
-    if (tid == 0 && grp + gridDim.x < a.ngroups) issue(grp + gridDim.x);
+    if constexpr (XC::OVL) {
+      if (tid == 0 && grp + gridDim.x < a.ngroups) issue(grp + gridDim.x);
+    }
     if (item < N * N) xld_z<N, Q>(Bv, a.E, grp, item, e, t);
     // (the next group's X stage writes only registers; its A writes come
     // after the barrier that follows its record reads, and Bv is rewritten

@@ -12,9 +12,20 @@ namespace tmop {
 #define TMOP_XLD_REG3 200
 #endif
 
+// group size of the p = 2 diagonal (0: the Hessian action's 8) and whether
+// the x^T output overlays the staged records (1) or has its own region (0:
+// the next group's record copy is then issued right after the X stage)
+#ifndef TMOP_XLD_EPB3
+#define TMOP_XLD_EPB3 0
+#endif
+#ifndef TMOP_XLD_OVL
+#define TMOP_XLD_OVL 1
+#endif
+
 template <int N, int Q>
 struct XldCfg {
-  static constexpr int EPB = xl_epb(N);
+  static constexpr int EPB = (N == 3 && TMOP_XLD_EPB3) ? TMOP_XLD_EPB3 : xl_epb(N);
+  static constexpr bool OVL = TMOP_XLD_OVL != 0;
   static constexpr int NP = N * N * N, QP = Q * Q * Q;
   static constexpr int LINES = Q * Q;
   static constexpr int NT = EPB * LINES;
@@ -23,10 +34,12 @@ struct XldCfg {
   static constexpr int A_SZ = NF * LINES * NA;          // slots (one slot = EPB doubles)
   static constexpr int NB = N * N;                      // Bv (ky, kx) plane
   static constexpr int BV_SZ = 9 * Q * NB;              // [c][g][qz][ky][kx]
-  static constexpr int QS = lean_stride(11 * QP, EPB);  // record element stride (doubles)
+  static constexpr int QS = lean_stride(11 * QP, xl_epb(N));   // record element stride (doubles)
   // A overlays the staged records (read-only during X; a barrier separates
-  // the last record read from the first A write), Bv has its own region
-  static constexpr int R1 = cmax(A_SZ * EPB, EPB * QS);
+  // the last record read from the first A write) or follows them (!OVL);
+  // Bv has its own region
+  static constexpr int AOFF = OVL ? 0 : ((EPB * QS + 1) & ~1);
+  static constexpr int R1 = OVL ? cmax(A_SZ * EPB, EPB * QS) : AOFF + A_SZ * EPB;
   static constexpr int R1P = (R1 + 1) & ~1;             // 16-byte aligned Bv
   static constexpr int SMEM = (R1P + BV_SZ * EPB) * 8;
   static constexpr int WARPS = (NT + 31) / 32;

@@ -725,7 +725,8 @@ def test_fused_setup_diagonal_equals_separate_passes(order, nq, metric, counts, 
     qa = p.hessian_setup(x)
     da = p.hessian_diagonal(qa)
     qb, db = p.hessian_setup_diagonal(x)
-    assert torch.equal(qa.data, qb.data)
+    used = p.qdata_fields * p.n_quad_total           # (the element stride's padding is never written)
+    assert torch.equal(qa.data[:, :used], qb.data[:, :used])
     assert torch.equal(da, db)
     op = O.OracleProblem(om, metric, nq)
     assert rel(db, op.hessian_diagonal(op.hessian_setup(x.cpu().numpy()))) <= TOL
@@ -743,7 +744,8 @@ for order, nq, counts in ((1, 3, (17, 3, 5)), (2, 4, (9, 7, 3)), (3, 5, (5, 3, 7
     x = torch.from_numpy(O.perturb(O.box_mesh(3, counts, order), np.random.default_rng(3), 0.2)).cuda()
     qa = p.hessian_setup(x); da = p.hessian_diagonal(qa)
     qb, db = p.hessian_setup_diagonal(x)
-    bad += int(not (torch.equal(qa.data, qb.data) and torch.equal(da, db)))
+    u = p.qdata_fields * p.n_quad_total
+    bad += int(not (torch.equal(qa.data[:, :u], qb.data[:, :u]) and torch.equal(da, db)))
 print("BAD", bad)
 """
 
