@@ -17,6 +17,10 @@
 
 namespace tmop {
 
+#ifndef TMOP_XL_GRAD_P3
+#define TMOP_XL_GRAD_P3 0
+#endif
+
 // TMOP_XL=0 forces the work-item kernels (elem_kernel) everywhere (A/B and
 // parity of the two implementations).
 inline bool xl_enabled() {
@@ -36,6 +40,9 @@ template <int N, int KIND>
 constexpr bool xl_kind() {
   if constexpr (KIND == K_SETUP_DIAG) return N <= 4;
   if constexpr (N >= 5) return KIND == K_ENERGY || KIND == K_MINDET;
+  // p = 3 gradient: the x-line form spills ~320 B per thread at 255
+  // registers; the work-item kernel measured faster (C3: 8.5 vs 9.1 ms)
+  if constexpr (N == 4 && KIND == K_GRAD) return TMOP_XL_GRAD_P3 != 0;
   return KIND == K_APPLY || KIND == K_APPLY_NT || KIND == K_GRAD || KIND == K_SETUP || KIND == K_ENERGY ||
          KIND == K_MINDET;
 }
