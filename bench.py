@@ -551,7 +551,7 @@ def slab_inputs(part, mesh, seed=SEED):
     return x, v
 
 
-def dist_leg(rank, world, device, counts, order, nq, steps, warmup, group=None, sampler=None):
+def dist_leg(rank, world, device, counts, order, nq, steps, warmup, group=None, sampler=None, transport="nccl"):
     """One distributed Hessian-action leg over z-slabs: the
     local action (slab-overlapped element kernel + E->L) then the halo plane
     sum + constraint re-fix (library pack / NCCL send-recv / unpack), timed
@@ -566,6 +566,8 @@ def dist_leg(rank, world, device, counts, order, nq, steps, warmup, group=None, 
     prob = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_303, P.TargetSpec(P.TargetKind.IDEAL_UNIT)), nq,
                          device=device)
     dp = DistributedProblem(prob, part, mesh.fixed_mask, group=group).to(device)
+    if transport == "p2p":
+        dp.enable_p2p()
     xh, vh_np = slab_inputs(part, mesh)
     x = torch.from_numpy(xh).to(device)
     v = torch.from_numpy(vh_np).to(device)
@@ -763,6 +765,20 @@ def run_distributed(args, rank, world, local, device, metric, config, group=None
     gc.collect()
     torch.cuda.empty_cache()
     c5 = None if args.no_newton else dist_c5(rank, world, device, args.dist_n or 96, group)
+    p2p = None
+    if world > 1:
+        # the same headline leg with the peer-memory halo (CUDA IPC mailboxes,
+        # stores over NVLink; no NCCL on the data path)
+        gc.collect()
+        torch.cuda.empty_cache()
+        try:
+            r, (prob2, dp2, _, _) = dist_leg(rank, world, device, (n2, n2, n2 * world), p2, q2, args.steps,
+                                             args.warmup, group, transport="p2p")
+            dp2.halo.check_p2p()
+            dp2.disable_p2p()
+            p2p = {k: r[k] for k in ("ms_per_step", "local_action_ms", "halo_ms_per_step", "gdofs")}
+        except Exception as err:   # reported, not fatal: NCCL legs above are the measurement
+            p2p = {"error": str(err)[:300]}
     if rank != 0:
         return
     peak = peaks()[0]
@@ -785,7 +801,7 @@ def run_distributed(args, rank, world, local, device, metric, config, group=None
                     "d2h_bytes_per_step": head["d2h_bytes_per_step"], "ms_per_step": head["e2e_ms_per_step"]},
             "gpu_launches": (2 * OVERLAP_SLABS + 2) * args.steps, "clocks": cs.summary(),
             "headline_leg": head, "c4_strong": strong, "c4_weak": weak, "newton_iteration": newton,
-            "c5_dist": c5,
+            "c5_dist": c5, "halo_p2p": p2p,
             "nccl": nccl_summary()}
     print(json.dumps(line))
 

@@ -307,6 +307,30 @@ int tmop_halo_pack(tmop_ctx *ctx, int64_t nn, int64_t plane, int lo, int hi, con
 int tmop_halo_unpack(tmop_ctx *ctx, int64_t nn, int64_t plane, int lo, int hi, const double *recv, int mode,
                      const double *vfix, double cfix, double *y);
 
+/* Peer-memory halo (no NCCL on the data path): each rank exports a mailbox
+ * box[2 slots][2 sides][3 x plane] doubles and two uint64 arrival counters
+ * cnt[2 sides] (side 0: from the lower neighbour, side 1: from the upper),
+ * and maps its neighbours' (CUDA IPC on one node; the stores travel over
+ * NVLink).  Exchange k (k = 1, 2, ...) uses slot k & 1:
+ *   put: this rank's bottom plane of y -> the lower neighbour's mailbox
+ *        (side 1), its top plane -> the upper neighbour's (side 0); every
+ *        CTA then releases one arrival at system scope on the receiver's
+ *        counter (tmop_halo_p2p_arrivals(plane) arrivals per exchange)
+ *   get: wait (acquire, bounded ~4 s -> *err = 1; once set, later gets
+ *        return at once) until the own counters
+ *        reach target = k * arrivals, then add the neighbours' partial sums
+ *        into y's planes and re-apply the constraint convention (mode as
+ *        tmop_halo_unpack).
+ * Both run on the context stream after the local E->L; no host round trip.
+ * Two slots suffice: a rank cannot start exchange k + 2 before its
+ * neighbours finished reading exchange k (each get waits on the other's put). */
+int tmop_halo_p2p_put(tmop_ctx *ctx, int64_t nn, int64_t plane, const double *y, double *peer_lo_box,
+                      uint64_t *peer_lo_cnt, double *peer_hi_box, uint64_t *peer_hi_cnt, int slot);
+int tmop_halo_p2p_get(tmop_ctx *ctx, int64_t nn, int64_t plane, double *y, const double *own_box,
+                      const uint64_t *own_cnt, int lo, int hi, int slot, uint64_t target, int mode,
+                      const double *vfix, double cfix, int32_t *err);
+int64_t tmop_halo_p2p_arrivals(int64_t plane);
+
 #ifdef __cplusplus
 }
 #endif

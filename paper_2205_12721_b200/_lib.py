@@ -87,10 +87,13 @@ _SIGS = {
     "tmop_minres_dist_k3": [_P, _I64, _P, _P, _P, _P, _P, _P, _D, _P, _INT, _P],
     "tmop_halo_pack": [_P, _I64, _I64, _INT, _INT, _P, _P],
     "tmop_halo_unpack": [_P, _I64, _I64, _INT, _INT, _P, _INT, _P, _D, _P],
+    "tmop_halo_p2p_put": [_P, _I64, _I64, _P, _P, _P, _P, _P, _INT],
+    "tmop_halo_p2p_get": [_P, _I64, _I64, _P, _P, _P, _INT, _INT, _INT, C.c_uint64, _INT, _P, _D, _P],
+    "tmop_halo_p2p_arrivals": [_I64],
     "tmop_last_error": [],
 }
 _RESTYPES = {"tmop_qdata_size": _I64, "tmop_qdata_stride": _I64, "tmop_last_error": C.c_char_p,
-             "tmop_ctx_point_scale": _P}
+             "tmop_ctx_point_scale": _P, "tmop_halo_p2p_arrivals": _I64}
 
 EXPORTED = tuple(_SIGS)
 

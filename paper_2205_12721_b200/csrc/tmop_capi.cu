@@ -829,6 +829,32 @@ int tmop_halo_unpack(tmop_ctx *c, int64_t nn, int64_t plane, int lo, int hi, con
   return TMOP_OK;
 }
 
+int tmop_halo_p2p_put(tmop_ctx *c, int64_t nn, int64_t plane, const double *y, double *peer_lo_box,
+                      uint64_t *peer_lo_cnt, double *peer_hi_box, uint64_t *peer_hi_cnt, int slot) {
+  if (!c || !y) return fail(TMOP_ERR_ARG, "NULL argument");
+  if ((peer_lo_box == nullptr) != (peer_lo_cnt == nullptr) || (peer_hi_box == nullptr) != (peer_hi_cnt == nullptr))
+    return fail(TMOP_ERR_ARG, "mailbox and counter must be given together");
+  if (slot < 0 || slot > 1 || plane <= 0 || plane > nn) return fail(TMOP_ERR_ARG, "slot / plane invalid");
+  launch_halo_p2p_put(nn, plane, y, peer_lo_box, reinterpret_cast<unsigned long long *>(peer_lo_cnt), peer_hi_box,
+                      reinterpret_cast<unsigned long long *>(peer_hi_cnt), slot, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int tmop_halo_p2p_get(tmop_ctx *c, int64_t nn, int64_t plane, double *y, const double *own_box,
+                      const uint64_t *own_cnt, int lo, int hi, int slot, uint64_t target, int mode,
+                      const double *vfix, double cfix, int32_t *err) {
+  if (!c || !y || !own_box || !own_cnt || !err) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (nn != c->nn) return fail(TMOP_ERR_ARG, "node count does not match the context");
+  if (slot < 0 || slot > 1 || plane <= 0 || plane > nn) return fail(TMOP_ERR_ARG, "slot / plane invalid");
+  launch_halo_p2p_get(nn, plane, y, own_box, reinterpret_cast<const unsigned long long *>(own_cnt), lo, hi, slot,
+                      (unsigned long long)target, c->fixed, mode, vfix, cfix, err, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  return TMOP_OK;
+}
+
+int64_t tmop_halo_p2p_arrivals(int64_t plane) { return halo_p2p_grid(plane); }
+
 int tmop_minres_set_history(tmop_ctx *c, double *hist, int capacity) {
   if (!c) return fail(TMOP_ERR_ARG, "ctx is NULL");
   c->hist = hist;

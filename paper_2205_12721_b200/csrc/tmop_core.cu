@@ -751,4 +751,91 @@ void launch_halo_unpack(int64_t nn, int64_t pl, int lo, int hi, const double *re
   if (g > 0) halo_unpack_kernel<<<g, 256, 0, s>>>(nn, pl, lo, hi, recv, fixed, mode, vfix, cfix, y);
 }
 
+// ---- peer-memory halo (tmop_halo_p2p_*): the shared planes go straight into
+// the neighbours' mailboxes (CUDA IPC / NVLink P2P stores), no NCCL on the
+// data path.  Mailbox: box[slot][side][3 pl] doubles, side 0 = from the
+// lower neighbour (its top plane), side 1 = from the upper neighbour (its
+// bottom plane); cnt[side] counts arrivals monotonically (one per put CTA).
+int halo_p2p_grid(int64_t pl) {
+  const int64_t g = (3 * pl + 255) / 256;
+  return (int)std::min<int64_t>(std::max<int64_t>(g, 1), 148 * 4);
+}
+
+__global__ void halo_p2p_put_kernel(int64_t nn, int64_t pl, const double *__restrict__ y, double *box_lo,
+                                    unsigned long long *cnt_lo, double *box_hi, unsigned long long *cnt_hi,
+                                    int slot) {
+  const int64_t tot = 3 * pl;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / pl, j = i - c * pl;
+    // my bottom plane -> the lower neighbour's side 1; my top plane -> the upper's side 0
+    if (box_lo) box_lo[(slot * 2 + 1) * tot + i] = y[c * nn + j];
+    if (box_hi) box_hi[(slot * 2 + 0) * tot + i] = y[c * nn + nn - pl + j];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (cnt_lo) asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(cnt_lo + 1) : "memory");
+    if (cnt_hi) asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(cnt_hi + 0) : "memory");
+  }
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void halo_p2p_get_kernel(int64_t nn, int64_t pl, double *__restrict__ y, const double *box,
+                                    const unsigned long long *cnt, int lo, int hi, int slot,
+                                    unsigned long long target, const uint8_t *__restrict__ fixed, int mode,
+                                    const double *__restrict__ vfix, double cfix, int *err) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    // bounded wait (~4 s): a missing neighbour reports an error instead of
+    // hanging the GPU, and every later exchange then returns at once
+    int good = *(volatile int *)err == 0;
+    for (int side = 0; side < 2 && good; ++side) {
+      if (side == 0 ? !lo : !hi) continue;
+      long long it = 0;
+      while (ld_acquire_sys(cnt + side) < target) {
+        __nanosleep(256);
+        if (++it > (1ll << 24)) {
+          good = 0;
+          atomicExch(err, 1);
+          break;
+        }
+      }
+    }
+    ok = good;
+  }
+  __syncthreads();
+  if (!ok) return;
+  const int64_t tot = 3 * pl;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / pl, j = i - c * pl;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      if (side == 0 ? !lo : !hi) continue;
+      const int64_t node = side == 0 ? j : nn - pl + j;
+      const int64_t k = c * nn + node;
+      double val = y[k] + __ldcg(box + (slot * 2 + side) * tot + i);
+      if (mode && ((__ldg(fixed + node) >> c) & 1)) val = vfix ? vfix[k] : cfix;
+      y[k] = val;
+    }
+  }
+}
+
+void launch_halo_p2p_put(int64_t nn, int64_t pl, const double *y, double *box_lo, unsigned long long *cnt_lo,
+                         double *box_hi, unsigned long long *cnt_hi, int slot, cudaStream_t s) {
+  halo_p2p_put_kernel<<<halo_p2p_grid(pl), 256, 0, s>>>(nn, pl, y, box_lo, cnt_lo, box_hi, cnt_hi, slot);
+}
+
+void launch_halo_p2p_get(int64_t nn, int64_t pl, double *y, const double *box, const unsigned long long *cnt, int lo,
+                         int hi, int slot, unsigned long long target, const uint8_t *fixed, int mode,
+                         const double *vfix, double cfix, int *err, cudaStream_t s) {
+  const int g = (int)std::min<int64_t>((3 * pl + 255) / 256, 148 * 4);
+  halo_p2p_get_kernel<<<g > 0 ? g : 1, 256, 0, s>>>(nn, pl, y, box, cnt, lo, hi, slot, target, fixed, mode, vfix,
+                                                    cfix, err);
+}
+
 }  // namespace tmop

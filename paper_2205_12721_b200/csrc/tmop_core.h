@@ -74,6 +74,12 @@ void launch_minres_dist_k3(int64_t n, const double *z, double *v, const double *
 void launch_halo_pack(int64_t nn, int64_t pl, int lo, int hi, const double *y, double *send, cudaStream_t s);
 void launch_halo_unpack(int64_t nn, int64_t pl, int lo, int hi, const double *recv, const uint8_t *fixed, int mode,
                         const double *vfix, double cfix, double *y, cudaStream_t s);
+int halo_p2p_grid(int64_t pl);
+void launch_halo_p2p_put(int64_t nn, int64_t pl, const double *y, double *box_lo, unsigned long long *cnt_lo,
+                         double *box_hi, unsigned long long *cnt_hi, int slot, cudaStream_t s);
+void launch_halo_p2p_get(int64_t nn, int64_t pl, double *y, const double *box, const unsigned long long *cnt, int lo,
+                         int hi, int slot, unsigned long long target, const uint8_t *fixed, int mode,
+                         const double *vfix, double cfix, int *err, cudaStream_t s);
 int launch_lattice_check(int64_t ne, int np, const int32_t *restr, int nx, int ny, int nz, int p, int *flag,
                          cudaStream_t s);
 

@@ -160,6 +160,69 @@ class HaloExchange:
                           torch.zeros(m, dtype=torch.float64, device=like.device))
         return self._bufs
 
+    # ---- peer-memory transport (tmop_halo_p2p_*): NVLink / CUDA IPC stores
+    # into the neighbours' mailboxes, stream-ordered, no NCCL on the data path
+    def enable_p2p(self, device):
+        """Allocate this rank's mailbox + arrival counters, export them by
+        CUDA IPC (torch.multiprocessing reductions) and map the neighbours'
+        (one node; ranks may share a GPU).  Collective over the group."""
+        torch = _torch()
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        pt = self.part
+        self.p2p_box = torch.zeros(2 * 2 * 3 * pt.plane, dtype=torch.float64, device=device)
+        self.p2p_cnt = torch.zeros(2, dtype=torch.int64, device=device)
+        self.p2p_err = torch.zeros(1, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        mine = (reduce_tensor(self.p2p_box), reduce_tensor(self.p2p_cnt))
+        objs = [None] * dist.get_world_size(self.group)
+        dist.all_gather_object(objs, mine, group=self.group)
+
+        def open_peer(r):
+            (fb, ab), (fc, ac) = objs[r]
+            return fb(*ab), fc(*ac)
+        self.p2p_lo = open_peer(pt.rank - 1) if pt.has_lower else (None, None)
+        self.p2p_hi = open_peer(pt.rank + 1) if pt.has_upper else (None, None)
+        self.p2p_epoch = 0
+        self.p2p_arrivals = int(self.lib.tmop_halo_p2p_arrivals(pt.plane))
+        dist.barrier(group=self.group)
+        self.p2p = True
+
+    def disable_p2p(self):
+        """Unmap the neighbours' mailboxes (collective: every rank must stop
+        using the peer memory before any rank frees its own)."""
+        import torch.distributed as dist
+        if not getattr(self, "p2p", False):
+            return
+        _torch().cuda.synchronize()
+        self.p2p = False
+        self.p2p_lo = self.p2p_hi = (None, None)
+        dist.barrier(group=self.group)
+
+    def check_p2p(self):
+        """Raise if a peer-memory exchange timed out (neighbour missing)."""
+        if getattr(self, "p2p", False) and int(self.p2p_err.item()):
+            raise RuntimeError("peer-memory halo exchange timed out (a neighbour did not deliver its plane)")
+
+    def _sum_planes_p2p(self, y, mode, vfix, cfix):
+        from . import _lib
+        pt = self.part
+        P = _lib.ptr
+        self.p2p_epoch += 1
+        slot = self.p2p_epoch & 1
+        lb, lc = self.p2p_lo
+        hb, hc = self.p2p_hi
+        _lib.check(self.lib.tmop_halo_p2p_put(self.ctx, pt.n_local, pt.plane, P(y), P(lb) if lb is not None else None,
+                                              P(lc) if lc is not None else None, P(hb) if hb is not None else None,
+                                              P(hc) if hc is not None else None, slot), "tmop_halo_p2p_put")
+        _lib.check(self.lib.tmop_halo_p2p_get(self.ctx, pt.n_local, pt.plane, P(y), P(self.p2p_box),
+                                              P(self.p2p_cnt), int(pt.has_lower), int(pt.has_upper), slot,
+                                              self.p2p_epoch * self.p2p_arrivals, int(mode),
+                                              P(vfix) if vfix is not None else None, float(cfix),
+                                              P(self.p2p_err)), "tmop_halo_p2p_get")
+        self.bytes_per_exchange = 3 * pt.plane * 8
+        return y
+
     def sum_planes_device(self, y, mode, vfix=None, cfix=0.0):
         """Device fast path: y (local T-vector on the GPU) receives the
         neighbours' partial sums on its planes; mode 1 re-fixes constrained
@@ -172,6 +235,8 @@ class HaloExchange:
         lo, hi = int(pt.has_lower), int(pt.has_upper)
         if not (lo or hi):
             return y
+        if getattr(self, "p2p", False):
+            return self._sum_planes_p2p(y, mode, vfix, cfix)
         send, recv = self._device_bufs(y)
         pl = pt.plane
         _lib.check(self.lib.tmop_halo_pack(self.ctx, pt.n_local, pl, lo, hi, _lib.ptr(y), _lib.ptr(send)),
@@ -361,6 +426,16 @@ class DistributedProblem:
             self.halo.sum_planes(y)
         return self.halo.refix(y, self.fixed2, v)
 
+    def disable_p2p(self):
+        self.halo.disable_p2p()
+
+    def enable_p2p(self):
+        """Switch the halo planes to the peer-memory transport (collective)."""
+        if not self.device_op:
+            raise ValueError("the peer-memory halo needs a device TmopProblem")
+        self.halo.enable_p2p(self.fixed2.device)
+        return self
+
     def hessian_apply_host(self, qdata, vh, out=None):
         """Host-resident action (pinned torch CPU v -> pinned y): the local
         slab runs the pipelined host path (H2D / element kernel + E->L / D2H
@@ -531,6 +606,7 @@ def dist_minres_device(problem: DistributedProblem, qdata, b, max_iterations=50,
             w1, w2, w = w2, w, w1
             k += 1
         s_ = state(k)
+        problem.halo.check_p2p()
         if s_["nonpd"]:
             raise ValueError("preconditioner is not positive definite")
         if s_["breakdown"]:

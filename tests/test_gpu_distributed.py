@@ -93,6 +93,16 @@ def _worker(rank, world, port, results):
         out["newton_alpha"] = ([r[0] for r in recs], [r.alpha for r in own.trace.records])
         out["newton_its"] = ([r[3] for r in recs], [r.minres_iterations for r in own.trace.records])
         out["newton_x"] = err(xn, np.asarray(own.x))
+        # peer-memory halo (CUDA IPC mailboxes, no NCCL / gloo on the data
+        # path): same plane sums -> bitwise the same results
+        dq = DistributedProblem(lp, part, lmesh.fixed_mask).to("cuda").enable_p2p()
+        out["p2p_apply"] = bool(torch.equal(dq.hessian_apply(lq, vl), ya))
+        out["p2p_grad"] = bool(torch.equal(dq.gradient(xl), dp.gradient(xl)))
+        out["p2p_diag"] = bool(torch.equal(dq.hessian_diagonal(lq), dp.hessian_diagonal(lq)))
+        xq, itq, _, _ = dist_minres_device(dq, lq, dq.gradient(xl), 20, 1e-300, linv)
+        out["p2p_minres"] = bool(torch.equal(xq, xdd)) and itq == itdd
+        dq.halo.check_p2p()
+        dq.disable_p2p()
         # size-field targets (mu_321) over the partition vs the global operator
         eta = P.size_field(gmesh, "shell")
         cfw = P.ObjectiveConfig(P.MetricId.MU_321, P.TargetSpec(P.TargetKind.SIZE_FIELD, size=eta))
@@ -105,6 +115,7 @@ def _worker(rank, world, port, results):
         out["size_grad"] = err(dw.gradient(xl), gw.gradient(x))
         out["size_obj"] = abs(dw.objective(xl) - gw.objective(x)) / abs(gw.objective(x))
         results[rank] = out
+        dist.barrier()
     finally:
         dist.destroy_process_group()
 
@@ -139,6 +150,7 @@ def test_slab_partition_with_device_operator_matches_global():
         assert out["newton_alpha"][0] == out["newton_alpha"][1], out
         assert out["newton_its"][0] == out["newton_its"][1], out
         assert out["newton_x"] <= 1e-9, out
+        assert out["p2p_apply"] and out["p2p_grad"] and out["p2p_diag"] and out["p2p_minres"], out
         assert out["size_apply"] <= 1e-13 and out["size_grad"] <= 1e-13 and out["size_obj"] <= 1e-13, out
 
 
