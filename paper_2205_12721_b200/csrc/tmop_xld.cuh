@@ -89,3 +89,4 @@ __global__ void __launch_bounds__(XldCfg<N, Q>::NT, XldCfg<N, Q>::MINB)
 }
 
 }  // namespace tmop
+
