@@ -181,8 +181,20 @@ class HaloExchange:
         def open_peer(r):
             (fb, ab), (fc, ac) = objs[r]
             return fb(*ab), fc(*ac)
-        self.p2p_lo = open_peer(pt.rank - 1) if pt.has_lower else (None, None)
-        self.p2p_hi = open_peer(pt.rank + 1) if pt.has_upper else (None, None)
+        err = None
+        try:
+            self.p2p_lo = open_peer(pt.rank - 1) if pt.has_lower else (None, None)
+            self.p2p_hi = open_peer(pt.rank + 1) if pt.has_upper else (None, None)
+        except Exception as e:       # (agree on failure below: no rank may leave the others waiting)
+            err = e
+            self.p2p_lo = self.p2p_hi = (None, None)
+        ok = torch.tensor([0.0 if err else 1.0], dtype=torch.float64)
+        if dist.get_backend(self.group) != "gloo":
+            ok = ok.to(device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        if float(ok.cpu()[0]) < 1.0:
+            self.p2p_lo = self.p2p_hi = (None, None)
+            raise RuntimeError(f"peer-memory halo unavailable on some rank ({err!r})")
         self.p2p_epoch = 0
         self.p2p_arrivals = int(self.lib.tmop_halo_p2p_arrivals(pt.plane))
         dist.barrier(group=self.group)
