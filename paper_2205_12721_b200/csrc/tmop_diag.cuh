@@ -119,22 +119,22 @@ __global__ void __launch_bounds__(ELEM_NT) diag2_kernel(const ElemArgs a, const 
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc) S[r][cc] = C[r][cc] * itau;
       if constexpr (!NTM) {
+        // regrouped as in xld_line (tmop_xld_parts.cuh): S_n u'_p + S_p u'_n,
+        // u'_k = 2 c1 T_k + (c2 + c3) S_k
         double c[4];
         lean_coeffs(a.metric, k0, itau, mfro2<DIM>(T), c);
-        const double c23 = c[2] + c[3];
+        const double c1x2 = 2.0 * c[1], c23 = c[2] + c[3];
 #pragma unroll
-        for (int cc = 0; cc < DIM; ++cc)
+        for (int cc = 0; cc < DIM; ++cc) {
+          double u[DIM];
+#pragma unroll
+          for (int k = 0; k < DIM; ++k) u[k] = c1x2 * T[cc][k] + c23 * S[cc][k];
 #pragma unroll
           for (int f = 0; f < NPAIR; ++f) {
             const int n = PR::n(f), p = PR::p(f);
-            const double sn = S[cc][n], sp = S[cc][p], tn = T[cc][n], tp = T[cc][p];
-            double v = c[1] * (sn * tp + tn * sp) + c23 * sn * sp;
-            if (n == p)
-              v += c[0];
-            else
-              v *= 2.0;
-            hp[(cc * NPAIR + f) * QP] = v;
+            hp[(cc * NPAIR + f) * QP] = (n == p) ? S[cc][n] * u[n] + c[0] : S[cc][n] * u[p] + S[cc][p] * u[n];
           }
+        }
       } else {
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc)

@@ -75,22 +75,24 @@ __device__ __forceinline__ void xld_line(int metric, const double *qb, const Tab
       for (int j = 0; j < 3; ++j) S[i][j] = C[i][j] * itau;
     double hv[3][6];
     if constexpr (!NTM) {
+      // c1 (S_n T_p + T_n S_p) + (c2 + c3) S_n S_p = S_n u_p + S_p u_n with
+      // u_k = c1 T_k + (c2 + c3)/2 S_k (operator.py:437-441 regrouped): the
+      // doubled off-diagonal pairs are S_n u'_p + S_p u'_n, u' = 2u, and the
+      // diagonal pairs S_n u'_n + c0 -- 21 instead of 36 FP64 ops per row
       double c[4];
       lean_coeffs(metric, k0, itau, mfro2<3>(T), c);
-      const double c23 = c[2] + c[3];
+      const double c1x2 = 2.0 * c[1], c23 = c[2] + c[3];
 #pragma unroll
-      for (int cc = 0; cc < 3; ++cc)
+      for (int cc = 0; cc < 3; ++cc) {
+        double u[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) u[k] = c1x2 * T[cc][k] + c23 * S[cc][k];
 #pragma unroll
         for (int f = 0; f < 6; ++f) {
           const int n = PR::n(f), p = PR::p(f);
-          const double sn = S[cc][n], sp = S[cc][p], tn = T[cc][n], tp = T[cc][p];
-          double v = c[1] * (sn * tp + tn * sp) + c23 * sn * sp;
-          if (n == p)
-            v += c[0];
-          else
-            v *= 2.0;
-          hv[cc][f] = v;
+          hv[cc][f] = (n == p) ? S[cc][n] * u[n] + c[0] : S[cc][n] * u[p] + S[cc][p] * u[n];
         }
+      }
     } else {
 #pragma unroll
       for (int cc = 0; cc < 3; ++cc)
