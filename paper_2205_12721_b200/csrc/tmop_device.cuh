@@ -379,6 +379,39 @@ __device__ __forceinline__ void nt_hess(int metric, double w, const double (&S)[
   }
 }
 
+// Row c of nt_hess for the unit direction g = e_c e_p^T (column (c, p) of
+// the Hessian block, the diagonal's need): with g a unit matrix the three
+// products of nt_hess collapse to rank-one terms,
+//   -dM[g]_cj = S_cp M_cj + (S S^T)_cc (S^T S)_pj + M_cp S_cj,
+// so a column costs ~15 FP64 operations instead of a full Hessian action.
+template <int D>
+struct NtDiag {
+  double SSt[D][D], StS[D][D], M[D][D], I1, J;
+  __device__ __forceinline__ NtDiag(const double (&S)[D][D], const double (&T)[D][D]) {
+    nt_sym<D>(S, SSt, StS);
+    mmul<D>(SSt, S, M);
+    I1 = mfro2<D>(T);
+    J = mfro2<D>(S);
+  }
+  // z[n] = H[(c,n),(c,p)] for n = 0..D-1 (metric MU302 / MU321, scale w)
+  __device__ __forceinline__ void col(int metric, double w, const double (&S)[D][D], const double (&T)[D][D], int c,
+                                      int p, double (&z)[D]) const {
+    double nM[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) nM[j] = S[c][p] * M[c][j] + SSt[c][c] * StS[p][j] + M[c][p] * S[c][j];
+    if (metric == MU302) {
+      const double cc = (2.0 / 9.0) * w;
+      const double dJ = -2.0 * M[c][p], dI1 = 2.0 * T[c][p];
+#pragma unroll
+      for (int j = 0; j < D; ++j) z[j] = cc * (dJ * T[c][j] + (j == p ? J : 0.0) - dI1 * M[c][j] + I1 * nM[j]);
+    } else {
+      const double cc = 2.0 * w;
+#pragma unroll
+      for (int j = 0; j < D; ++j) z[j] = cc * ((j == p ? 1.0 : 0.0) + nM[j]);
+    }
+  }
+};
+
 // ------------------------------------------- TMA bulk copy + mbarrier
 // One elected thread streams a contiguous global range into shared memory
 // with cp.async.bulk (the TMA engine, no register staging); consumers wait

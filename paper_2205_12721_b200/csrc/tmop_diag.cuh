@@ -136,17 +136,17 @@ __global__ void __launch_bounds__(ELEM_NT) diag2_kernel(const ElemArgs a, const 
           }
         }
       } else {
+        const NtDiag<DIM> nd(S, T);             // column (c,p): z[n] = H[(c,n),(c,p)] (unit-direction nt_hess)
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc)
 #pragma unroll
           for (int p = 0; p < DIM; ++p) {
-            double g[DIM][DIM] = {}, z[DIM][DIM];
-            g[cc][p] = 1.0;
-            nt_hess<DIM>(a.metric, k0, S, T, g, z);   // column (c,p) of the block: z[c][n] = H[(c,n),(c,p)]
+            double z[DIM];
+            nd.col(a.metric, k0, S, T, cc, p, z);
 #pragma unroll
             for (int f = 0; f < NPAIR; ++f) {
               const int n = PR::n(f), pp = PR::p(f);
-              if (pp == p) hp[(cc * NPAIR + f) * QP] = (n == p) ? z[cc][n] : 2.0 * z[cc][n];
+              if (pp == p) hp[(cc * NPAIR + f) * QP] = (n == p) ? z[n] : 2.0 * z[n];
             }
           }
       }

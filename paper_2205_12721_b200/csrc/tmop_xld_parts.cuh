@@ -94,17 +94,17 @@ __device__ __forceinline__ void xld_line(int metric, const double *qb, const Tab
         }
       }
     } else {
+      const NtDiag<3> nd(S, T);               // column (c,p): z[n] = H[(c,n),(c,p)] (unit-direction nt_hess)
 #pragma unroll
       for (int cc = 0; cc < 3; ++cc)
 #pragma unroll
         for (int p = 0; p < 3; ++p) {
-          double g[3][3] = {}, z[3][3];
-          g[cc][p] = 1.0;
-          nt_hess<3>(metric, k0, S, T, g, z);   // column (c,p) of the block: z[c][n] = H[(c,n),(c,p)]
+          double z[3];
+          nd.col(metric, k0, S, T, cc, p, z);
 #pragma unroll
           for (int f = 0; f < 6; ++f) {
             const int n = PR::n(f), pp = PR::p(f);
-            if (pp == p) hv[cc][f] = (n == p) ? z[cc][n] : 2.0 * z[cc][n];
+            if (pp == p) hv[cc][f] = (n == p) ? z[n] : 2.0 * z[n];
           }
         }
     }
