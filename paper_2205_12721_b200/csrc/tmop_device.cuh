@@ -344,24 +344,40 @@ __device__ __forceinline__ void nt_first(int metric, const double (&T)[D][D], co
 template <int D>
 __device__ __forceinline__ void nt_hess(int metric, double w, const double (&S)[D][D], const double (&T)[D][D],
                                         const double (&g)[D][D], double (&z)[D][D]) {
-  double SSt[D][D], StS[D][D], M[D][D];
+  // -dM[g] = S g^T M + S S^T g S^T S + M g^T S with M = S S^T S regrouped as
+  //   B = S (g^T S):  -dM[g] = B (S^T S) + (S S^T)(g S^T S + B)
+  // -- five 3x3 products instead of six plus M (M itself only for mu_302)
+  double SSt[D][D], StS[D][D];
   nt_sym<D>(S, SSt, StS);
-  mmul<D>(SSt, S, M);
-  double X[D][D], Y[D][D], Z[D][D];
-  mmulT<D>(S, g, X);             // S g^T
-  mmul<D>(SSt, g, Y);            // S S^T g
-  mmulT<D>(M, g, Z);             // M g^T
+  double A[D][D], B[D][D], Cm[D][D];
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double s0 = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) s0 += g[k][i] * S[k][j];
+      A[i][j] = s0;                       // g^T S
+    }
+  mmul<D>(S, A, B);
+  mmul<D>(g, StS, Cm);
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) Cm[i][j] += B[i][j];
   double nM[D][D];               // -dM[g]
 #pragma unroll
   for (int i = 0; i < D; ++i)
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      double s = 0.0;
+      double s0 = 0.0;
 #pragma unroll
-      for (int k = 0; k < D; ++k) s += X[i][k] * M[k][j] + Y[i][k] * StS[k][j] + Z[i][k] * S[k][j];
-      nM[i][j] = s;
+      for (int k = 0; k < D; ++k) s0 += B[i][k] * StS[k][j] + SSt[i][k] * Cm[k][j];
+      nM[i][j] = s0;
     }
   if (metric == MU302) {
+    double M[D][D];
+    mmul<D>(SSt, S, M);
     const double I1 = mfro2<D>(T), J = mfro2<D>(S);
     const double dJ = -2.0 * mdot<D>(M, g), dI1 = 2.0 * mdot<D>(T, g);
     const double c = (2.0 / 9.0) * w;
