@@ -84,7 +84,7 @@ FP64_PEAK_TFLOPS = 37.1   # measured on this pool's B200: DMMA loop 37.1, DFMA l
 
 def measured_traffic(key):
     try:
-        with open(os.path.join(ROOT, "profiles", "round1_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "round2_traffic.json")) as f:
             t = json.load(f)[key]
         return t["dram_bytes_read"] + t["dram_bytes_write"], t
     except Exception:
@@ -969,7 +969,7 @@ def main():
                      "algorithmic_bytes_per_launch": head["elem_bytes"],
                      "bytes_note": "algorithmic = reference-format Q-data (22 fp64/point) + restriction + v + "
                                    "E-vector write (SURVEY 8(d)); the kernel streams the lean 11-fp64 record, so "
-                                   "frac > 1 is possible -- traffic (ncu dram bytes, profiles/round1_traffic.json) "
+                                   "frac > 1 is possible -- traffic (ncu dram bytes, profiles/round2_traffic.json) "
                                    "is what it actually moves",
                      "traffic_frac_of_peak": (traffic / (head["t_elem_ms"] / 1e3) / 1e9 / peak) if traffic else None,
                      "kernel_share_of_step": head["t_elem_ms"] / head["ms_per_step"],
