@@ -270,22 +270,39 @@ __device__ __forceinline__ void xl_point_x(const ElemArgs &a, const Tab &t, int6
     const PtScale ps = pt_scale<3>(a, (eg < a.ne ? eg : 0) * QP + q);
     const double tau = dj * ps.is_d;
     const double I1 = mfro2<3>(J) * (ps.is * ps.is);
-    const double itau = 1.0 / tau;   // the one division of the point
-    const double cs = ps.is_dm1 * itau;
-    double Cof[3][3];
-    mcof<3>(J, Cof);
-    double S[3][3], T[3][3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        S[i][j] = cs * Cof[i][j];
-        T[i][j] = ps.is * J[i][j];
-      }
     const double wpt = wq<3, Q>(t, q);
+    // S = cof(T) / det T and T itself only where the metric / kind reads them
+    // (the template metrics' energy and gradient need neither)
+    auto mk_s = [&](const double (&Cof)[3][3], double cs, double (&S)[3][3]) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) S[i][j] = cs * Cof[i][j];
+    };
+    auto mk_t = [&](double (&T)[3][3]) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) T[i][j] = ps.is * J[i][j];
+    };
+    const bool uses_s = a.metric == MU7 || !metric_is_template(a.metric);
     if constexpr (KIND == K_ENERGY) {
-      if (eg < a.ne) acc += (wpt * ps.ew) * metric_mu<3>(a.metric, tau, I1, S);
+      double mu;
+      if (uses_s) {
+        const double itau = 1.0 / tau;
+        double Cof[3][3], S[3][3];
+        mcof<3>(J, Cof);
+        mk_s(Cof, ps.is_dm1 * itau, S);
+        mu = metric_mu<3>(a.metric, tau, I1, S);
+      } else {
+        const double Z[3][3] = {};
+        mu = metric_mu<3>(a.metric, tau, I1, Z);
+      }
+      if (eg < a.ne) acc += (wpt * ps.ew) * mu;
     } else if constexpr (KIND == K_SETUP) {
+      const double itau = 1.0 / tau;   // the one division of the point
+      double T[3][3];
+      mk_t(T);
       // lean record (operator.py:350-371 restated; see lean_k0), staged in
       // shared memory at slot = line + Q^2 qx of this thread's element
       double *qo = rec + line + Q * Q * qx;
@@ -296,12 +313,23 @@ __device__ __forceinline__ void xl_point_x(const ElemArgs &a, const Tab &t, int6
       qo[9 * QP] = lean_k0(a.metric, ps.ch * wpt, tau);
       qo[10 * QP] = itau;
     } else {  // K_GRAD: P = cw (a_t T + a_s S) (operator.py:328-346), + the energy
+      const double itau = 1.0 / tau;
+      const double cs = ps.is_dm1 * itau;
+      double Cof[3][3];
+      mcof<3>(J, Cof);
       const double cw = ps.cg * wpt;
       const bool en = a.energy && eg < a.ne;   // (line-search evaluation)
       double P[3][3];
       if (metric_is_template(a.metric)) {
         double at, as, mu = 0.0;
-        metric_mu_first<3>(a.metric, tau, I1, S, en, mu, at, as);
+        if (uses_s && en) {
+          double S[3][3];
+          mk_s(Cof, cs, S);
+          metric_mu_first<3>(a.metric, tau, I1, S, en, mu, at, as);
+        } else {
+          const double Z[3][3] = {};
+          metric_mu_first<3>(a.metric, tau, I1, Z, en, mu, at, as);
+        }
         if (en) acc += (wpt * ps.ew) * mu;
         const double ct = cw * at * ps.is;
         const double cc = cw * as * ps.is_dm1 * itau;
@@ -310,6 +338,9 @@ __device__ __forceinline__ void xl_point_x(const ElemArgs &a, const Tab &t, int6
 #pragma unroll
           for (int j = 0; j < 3; ++j) P[i][j] = ct * J[i][j] + cc * Cof[i][j];
       } else {
+        double S[3][3], T[3][3];
+        mk_s(Cof, cs, S);
+        mk_t(T);
         if (en) acc += (wpt * ps.ew) * metric_mu<3>(a.metric, tau, I1, S);
         nt_first<3>(a.metric, T, S, P);
 #pragma unroll
