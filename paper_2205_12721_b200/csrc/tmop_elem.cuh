@@ -774,31 +774,57 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::template m
           const double I1 = mfro2<DIM>(A) * (ps.is * ps.is);
           const double itau = 1.0 / tau;   // the one division of the point
           const double cs = ps.is_dm1 * itau;
-          double Cof[DIM][DIM];
-          mcof<DIM>(A, Cof);
-          double S[DIM][DIM], T[DIM][DIM];
-#pragma unroll
-          for (int i = 0; i < DIM; ++i)
-#pragma unroll
-            for (int j = 0; j < DIM; ++j) {
-              S[i][j] = cs * Cof[i][j];
-              T[i][j] = ps.is * A[i][j];
-            }
           const double wpt = wq<DIM, Q>(t, q);
+          // S = cof(T) / det T and T only where the metric / kind reads them
+          // (the template metrics' energy and gradient need neither)
+          const bool uses_s = a.metric == MU7 || !metric_is_template(a.metric);
+          auto mk_s = [&](const double (&Cof)[DIM][DIM], double (&S)[DIM][DIM]) {
+#pragma unroll
+            for (int i = 0; i < DIM; ++i)
+#pragma unroll
+              for (int j = 0; j < DIM; ++j) S[i][j] = cs * Cof[i][j];
+          };
+          auto mk_t = [&](double (&T)[DIM][DIM]) {
+#pragma unroll
+            for (int i = 0; i < DIM; ++i)
+#pragma unroll
+              for (int j = 0; j < DIM; ++j) T[i][j] = ps.is * A[i][j];
+          };
           if constexpr (KIND == K_ENERGY) {
-            acc += (wpt * ps.ew) * metric_mu<DIM>(a.metric, tau, I1, S);
+            double mu;
+            if (uses_s) {
+              double Cof[DIM][DIM], S[DIM][DIM];
+              mcof<DIM>(A, Cof);
+              mk_s(Cof, S);
+              mu = metric_mu<DIM>(a.metric, tau, I1, S);
+            } else {
+              const double Z[DIM][DIM] = {};
+              mu = metric_mu<DIM>(a.metric, tau, I1, Z);
+            }
+            acc += (wpt * ps.ew) * mu;
           } else if constexpr (KIND == K_SETUP) {
             // lean record (operator.py:350-371 restated; see lean_k0)
+            double T[DIM][DIM];
+            mk_t(T);
             double *qo = a.qout + eg * QS + lean_slot<DIM, Q>(q);
             store_point<DIM>(qo, QP, T);
             qo[DIM * DIM * QP] = lean_k0(a.metric, ps.ch * wpt, tau);
             qo[(DIM * DIM + 1) * QP] = itau;
           } else {  // K_GRAD (+ the energy, for the fused line-search evaluation)
+            double Cof[DIM][DIM];
+            mcof<DIM>(A, Cof);
             const double cw = ps.cg * wpt;
             double P[DIM][DIM];
             if (metric_is_template(a.metric)) {
               double at, as, mu = 0.0;
-              metric_mu_first<DIM>(a.metric, tau, I1, S, a.energy, mu, at, as);
+              if (uses_s && a.energy) {
+                double S[DIM][DIM];
+                mk_s(Cof, S);
+                metric_mu_first<DIM>(a.metric, tau, I1, S, a.energy, mu, at, as);
+              } else {
+                const double Z[DIM][DIM] = {};
+                metric_mu_first<DIM>(a.metric, tau, I1, Z, a.energy, mu, at, as);
+              }
               if (a.energy) acc += (wpt * ps.ew) * mu;
               const double ct = cw * at * ps.is;
               const double cc = cw * as * ps.is_dm1 * itau;
@@ -807,6 +833,9 @@ __global__ void __launch_bounds__(Cfg<DIM, N, Q>::NT, Cfg<DIM, N, Q>::template m
 #pragma unroll
                 for (int j = 0; j < DIM; ++j) P[i][j] = ct * A[i][j] + cc * Cof[i][j];
             } else {
+              double S[DIM][DIM], T[DIM][DIM];
+              mk_s(Cof, S);
+              mk_t(T);
               if (a.energy) acc += (wpt * ps.ew) * metric_mu<DIM>(a.metric, tau, I1, S);
               nt_first<DIM>(a.metric, T, S, P);
 #pragma unroll
