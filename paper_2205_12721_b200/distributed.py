@@ -206,10 +206,14 @@ class HaloExchange:
         import torch.distributed as dist
         if not getattr(self, "p2p", False):
             return
-        _torch().cuda.synchronize()
+        torch = _torch()
+        torch.cuda.synchronize()
         self.p2p = False
         self.p2p_lo = self.p2p_hi = (None, None)
+        import gc
+        gc.collect()                  # drop the mapped peer storages now ...
         dist.barrier(group=self.group)
+        torch.cuda.ipc_collect()      # ... so each producer can release its exported ones
 
     def check_p2p(self):
         """Raise if a peer-memory exchange timed out (neighbour missing)."""
