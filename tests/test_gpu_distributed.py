@@ -120,19 +120,21 @@ def _worker(rank, world, port, results):
         dist.destroy_process_group()
 
 
-def test_slab_partition_with_device_operator_matches_global():
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_partition_with_device_operator_matches_global(world):
+    """world 3: the middle rank has both neighbours (two planes per exchange)."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     results = mgr.dict()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, results)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, results)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(600)
+        p.join(900)
         assert p.exitcode == 0
-    for r in range(2):
+    for r in range(world):
         out = results[r]
         assert out["lattice"], out
         assert out["apply"] <= 1e-13, out
