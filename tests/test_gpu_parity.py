@@ -751,3 +751,27 @@ def test_fused_setup_diagonal_kernel_is_bitwise_equal():
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "BAD 0" in r.stdout, r.stdout
+
+
+def test_size_field_newton_matches_oracle(rng):
+    """C5-type solve (mu_321 with size-field targets) on a small mesh: the
+    device newton_solve against the oracle's restatement of the reference
+    Newton loop (sol:263-321) with the same targets -- alpha and MINRES
+    counts exact, iterates to 1e-9 (extension: the oracle's size-field
+    operator is FD / PA-vs-FA checked, tests/test_oracle.py)."""
+    import paper_2205_12721_b200 as P
+    counts, order, nq = (4, 3, 3), 2, 4
+    mesh = P.build_box(3, counts, order)
+    om = O.box_mesh(3, counts, order)
+    eta = P.size_field(mesh, "shell")
+    p = P.TmopProblem(mesh, P.ObjectiveConfig(P.MetricId.MU_321, P.TargetSpec(P.TargetKind.SIZE_FIELD, size=eta)),
+                      nq)
+    op = O.OracleProblem(om, O.MU_321, nq, target="field", size=eta)
+    x0 = O.perturb(om, rng, 0.2)
+    res = P.newton_solve(x0, p, P.NewtonConfig(max_iterations=3), P.MinresConfig())
+    xo, recs, ok, relg, g0, msg = O.newton(x0, op, max_it=3)
+    assert [r.alpha for r in res.trace.records] == [r[0] for r in recs]
+    assert [r.minres_iterations for r in res.trace.records] == [r[3] for r in recs]
+    for r, o in zip(res.trace.records, recs):
+        assert r.objective == pytest.approx(o[1], rel=1e-9)
+    assert rel(res.x, xo) <= 1e-9
