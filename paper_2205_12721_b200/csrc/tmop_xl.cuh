@@ -74,6 +74,13 @@ struct XlPad {
                                        : (N == 4 ? Q * 5 : (Q == 3 ? 21 : Q == 4 ? 21 : Q == 6 ? 33 : Q * W_QY));
 };
 
+// software prefetch of the next point's record fields in the x-line apply
+// (registers): -1 = per order (measured at C3: p = 3 6.81 -> 5.78 ms element
+// kernel; p = 2 slower, 7.27 -> 7.58 ms; p = 1 slower, 6.6 -> 8.1 ms), 0 = never, 1 = always
+#ifndef TMOP_XL_QPF
+#define TMOP_XL_QPF -1
+#endif
+
 #ifndef TMOP_XL_GRAD_MINB
 #define TMOP_XL_GRAD_MINB 0
 #endif
@@ -546,6 +553,9 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
         }
       }
 #pragma unroll
+      constexpr bool QPF = APPLY && (TMOP_XL_QPF == 1 || (TMOP_XL_QPF == -1 && N == 4));
+      double qnext[11];
+      if constexpr (QPF) qload(0, qnext);
       for (int qx = 0; qx < Q; ++qx) {
         double tg[N], tb[N];
 #pragma unroll
@@ -569,7 +579,14 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
         }
         if constexpr (APPLY) {
           double qd[11];
-          qload(qx, qd);
+          if constexpr (QPF) {
+            // this point's record was loaded during the previous point; fetch the next one now
+#pragma unroll
+            for (int f = 0; f < 11; ++f) qd[f] = qnext[f];
+            if (qx + 1 < Q) qload(qx + 1, qnext);
+          } else {
+            qload(qx, qd);
+          }
           xl_point<N, NTM>(a.metric, qd, g, tg, tb, av);
         } else {
           xl_point_x<SD ? K_SETUP : KIND, N, Q>(a, t, eg, line, qx, g, tg, tb, av, acc, mn, QS_rec);
