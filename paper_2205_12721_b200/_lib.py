@@ -85,6 +85,7 @@ _SIGS = {
     "tmop_minres_dist_k1": [_P, _I64, _I64, _I64, _P, _P, _P, _P, _INT, _P],
     "tmop_minres_dist_k2": [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _INT, _P],
     "tmop_minres_dist_k3": [_P, _I64, _P, _P, _P, _P, _P, _P, _D, _P, _INT, _P],
+    "tmop_copy_components": [_P, _P, _P, _I64, _I64, _I64, _INT],
     "tmop_halo_pack": [_P, _I64, _I64, _INT, _INT, _P, _P],
     "tmop_halo_unpack": [_P, _I64, _I64, _INT, _INT, _P, _INT, _P, _D, _P],
     "tmop_halo_p2p_put": [_P, _I64, _I64, _P, _P, _P, _P, _P, _INT],

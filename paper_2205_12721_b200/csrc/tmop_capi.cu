@@ -811,6 +811,18 @@ int tmop_minres_dist_k3(tmop_ctx *c, int64_t n, const double *z, double *v, cons
   return TMOP_OK;
 }
 
+int tmop_copy_components(tmop_ctx *c, double *dst, const double *src, int64_t stride, int64_t begin, int64_t count,
+                         int ncomp) {
+  if (!c || !dst || !src) return fail(TMOP_ERR_ARG, "NULL argument");
+  if (ncomp < 1 || begin < 0 || count < 0 || begin + count > stride)
+    return fail(TMOP_ERR_ARG, "range [%lld, %lld) outside the component stride %lld", (long long)begin,
+                (long long)(begin + count), (long long)stride);
+  if (count == 0) return TMOP_OK;
+  CUDA_TRY(cudaMemcpy2DAsync(dst + begin, (size_t)stride * 8, src + begin, (size_t)stride * 8, (size_t)count * 8,
+                             (size_t)ncomp, cudaMemcpyDefault, c->stream));
+  return TMOP_OK;
+}
+
 int tmop_halo_pack(tmop_ctx *c, int64_t nn, int64_t plane, int lo, int hi, const double *y, double *send) {
   if (!c || !y || !send) return fail(TMOP_ERR_ARG, "NULL argument");
   if (plane < 0 || 2 * plane > nn + plane) return fail(TMOP_ERR_ARG, "plane size invalid");

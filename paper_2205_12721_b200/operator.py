@@ -584,7 +584,6 @@ class TmopProblem:
         caller = torch.cuda.current_stream(self.device)
         vt = torch.empty(m.n_dofs, dtype=torch.float64, device=self.device)
         y = torch.empty_like(vt)
-        V, Y, VH, OH = vt.view(3, nn), y.view(3, nn), vh.view(3, nn), out.view(3, nn)
         for s_ in pipe:
             s_.wait_stream(caller)
 
@@ -616,8 +615,9 @@ class TmopProblem:
             hi = node_hi(e1 - 1)
             with torch.cuda.stream(h2d):
                 if hi > copied:
-                    for c in range(3):
-                        V[c, copied:hi].copy_(VH[c, copied:hi], non_blocking=True)
+                    self._sync_stream()
+                    _lib.check(self.lib.tmop_copy_components(self._ctx, _lib.ptr(vt), _lib.ptr(vh), nn, copied,
+                                                             hi - copied, 3), "tmop_copy_components")
                     copied = hi
             comp.wait_stream(h2d)
             fin = nn if e1 == ne else (e1 // layer) * p * NX * NY
@@ -631,8 +631,9 @@ class TmopProblem:
             d2h.wait_stream(comp)
             if fin > done:
                 with torch.cuda.stream(d2h):
-                    for c in range(3):
-                        OH[c, done:fin].copy_(Y[c, done:fin], non_blocking=True)
+                    self._sync_stream()
+                    _lib.check(self.lib.tmop_copy_components(self._ctx, _lib.ptr(out), _lib.ptr(y), nn, done,
+                                                             fin - done, 3), "tmop_copy_components")
                 done = fin
         d2h.synchronize()
         vt.record_stream(comp)
