@@ -158,7 +158,7 @@ int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
       // and the records-overlay layout: tuning variants that change either
       // keep the two passes)
       if constexpr (DIM == 3 && xl_kind<N, KIND>() && XlCfg<N, Q>::template smem<KIND>() <= 227 * 1024 &&
-                    XldCfg<N, Q>::EPB == XlCfg<N, Q>::EPB && XldCfg<N, Q>::OVL) {
+                    XldCfg<N, Q>::EPB == XlCfg<N, Q>::EPB) {
         if (xl_enabled() && xld_enabled()) return launch_xl<N, Q, KIND>(a, t, s);
       }
       return -1;

@@ -123,7 +123,7 @@ struct XlCfg {
   static constexpr int SMEM_S = (QOFF_S + EPB * QS) * 8;
   // setup + diagonal: the diagonal's x^T output A overlays the group's
   // records once they are stored (XldCfg::R1), its y^T output Bv follows
-  static constexpr int SMEM_SD = (QOFF_S + XldCfg<N, Q>::R1P + XldCfg<N, Q>::BV_SZ * EPB) * 8;
+  static constexpr int SMEM_SD = (QOFF_S + XldCfg<N, Q>::R1OP + XldCfg<N, Q>::BV_SZ * EPB) * 8;
   template <int KIND>
   static constexpr int smem() {
     return xl_qdata<KIND>() ? SMEM
@@ -676,9 +676,9 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
       __syncthreads();                  // ... and so has every thread: A may overlay it
       xld_store_a<N, Q>(QB, line, e, dacc);
       __syncthreads();
-      if (item < Q * N) xld_y<N, Q>(QB, QB + XldCfg<N, Q>::R1P, item, e, t);
+      if (item < Q * N) xld_y<N, Q>(QB, QB + XldCfg<N, Q>::R1OP, item, e, t);
       __syncthreads();
-      if (item < N * N) xld_z<N, Q>(QB + XldCfg<N, Q>::R1P, a.E, grp, item, e, t);
+      if (item < N * N) xld_z<N, Q>(QB + XldCfg<N, Q>::R1OP, a.E, grp, item, e, t);
     }
     // (no end-of-group barrier: the top-of-loop barrier orders this group's
     // reads of U / Bv before the next F1 writes U)

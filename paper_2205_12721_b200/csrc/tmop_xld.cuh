@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(XldCfg<N, Q>::NT, XldCfg<N, Q>::MINB)
   extern __shared__ __align__(16) double smem[];
   double *QB = smem;                           // staged records ...
   double *A = smem + XC::AOFF;                 // ... overlaid by the x^T output (OVL) or beside them
-  double *Bv = smem + XC::R1P;
+  double *Bv = XC::BVA ? A : smem + XC::R1P;    // (BVA: inside A's consumed slots)
   __shared__ __align__(8) uint64_t qbar;
 
   const int tid = threadIdx.x;
@@ -75,12 +75,12 @@ __global__ void __launch_bounds__(XldCfg<N, Q>::NT, XldCfg<N, Q>::MINB)
     }
     xld_store_a<N, Q>(A, item, e, acc);
     __syncthreads();
-    if (item < Q * N) xld_y<N, Q>(A, Bv, item, e, t);
+    if (item < Q * N) xld_y<N, Q, XC::BVA>(A, Bv, item, e, t);
     __syncthreads();                           // A (= QB) consumed: stream in the next group's records
     if constexpr (XC::OVL) {
       if (tid == 0 && grp + gridDim.x < a.ngroups) issue(grp + gridDim.x);
     }
-    if (item < N * N) xld_z<N, Q>(Bv, a.E, grp, item, e, t);
+    if (item < N * N) xld_z<N, Q, XC::BVA>(Bv, a.E, grp, item, e, t);
     // (the next group's X stage writes only registers; its A writes come
     // after the barrier that follows its record reads, and Bv is rewritten
     // only after the next Y barrier -- Z of this group is ordered before

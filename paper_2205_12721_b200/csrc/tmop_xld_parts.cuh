@@ -21,11 +21,20 @@ namespace tmop {
 #ifndef TMOP_XLD_OVL
 #define TMOP_XLD_OVL 1
 #endif
+// p <= 2: the records keep their own region, the x^T output A follows them
+// and the y^T output Bv is written into A's own consumed slots (item (qz,kx)
+// reads only A[.][.][qz][.][kx]), so the next group's record copy is issued
+// right after the X stage and lands during the A store / Y / Z stages, in
+// 100 KB per CTA at p = 2 (2 CTAs / SM, like the overlay layout)
+#ifndef TMOP_XLD_BVA
+#define TMOP_XLD_BVA 1
+#endif
 
 template <int N, int Q>
 struct XldCfg {
   static constexpr int EPB = (N == 3 && TMOP_XLD_EPB3) ? TMOP_XLD_EPB3 : xl_epb(N);
-  static constexpr bool OVL = TMOP_XLD_OVL != 0;
+  static constexpr bool BVA = TMOP_XLD_BVA != 0 && N <= 3;
+  static constexpr bool OVL = !BVA && TMOP_XLD_OVL != 0;
   static constexpr int NP = N * N * N, QP = Q * Q * Q;
   static constexpr int LINES = Q * Q;
   static constexpr int NT = EPB * LINES;
@@ -41,9 +50,15 @@ struct XldCfg {
   static constexpr int AOFF = OVL ? 0 : ((EPB * QS + 1) & ~1);
   static constexpr int R1 = OVL ? cmax(A_SZ * EPB, EPB * QS) : AOFF + A_SZ * EPB;
   static constexpr int R1P = (R1 + 1) & ~1;             // 16-byte aligned Bv
-  static constexpr int SMEM = (R1P + BV_SZ * EPB) * 8;
+  static constexpr int SMEM = (R1P + (BVA ? 0 : BV_SZ * EPB)) * 8;
+  // the fused setup + diagonal kind (xl_kernel<K_SETUP_DIAG>) always lays A
+  // over its records and Bv after them
+  static constexpr int R1OP = (cmax(A_SZ * EPB, EPB * QS) + 1) & ~1;
   static constexpr int WARPS = (NT + 31) / 32;
-  static constexpr int MINB = cmax(1, 65536 / (WARPS * 32 * (N <= 2 ? 128 : N == 3 ? TMOP_XLD_REG3 : 240)));
+  // occupancy hint: the register target per order, but no more CTAs than
+  // fit in shared memory (BVA p = 1: 2 CTAs, so no 128-register cap / spill)
+  static constexpr int MINB = cmax(1, cmin(65536 / (WARPS * 32 * (N <= 2 ? 128 : N == 3 ? TMOP_XLD_REG3 : 240)),
+                                           (228 * 1024) / (SMEM + 1024 + 1024)));
 };
 
 // X: the 18 H-pair values of every point of this thread's line (template or
@@ -132,8 +147,8 @@ __device__ __forceinline__ void xld_store_a(double *A, int line, int e, const do
 
 // Y: item (qz, kx) -- y^T sweep of every pair, pairs with equal z table
 // summed (Pairs::zgroup): Bv[c][g][qz][ky][kx]
-template <int N, int Q>
-__device__ __forceinline__ void xld_y(const double *A, double *Bv, int item, int e, const Tab &t) {
+template <int N, int Q, bool BVA = false>
+__device__ __forceinline__ void xld_y(double *A, double *Bv, int item, int e, const Tab &t) {
   using XC = XldCfg<N, Q>;
   using PR = Pairs<3>;
   constexpr int EPB = XC::EPB, NA = XC::NA, NB = XC::NB, AV = XC::LINES * NA * EPB;
@@ -163,17 +178,26 @@ __device__ __forceinline__ void xld_y(const double *A, double *Bv, int item, int
 #pragma unroll
     for (int g = 0; g < 3; ++g)
 #pragma unroll
-      for (int k = 0; k < N; ++k) Bv[(cc * 3 + g) * BG + y_qz * BQ + (k * N + y_kx) * EPB + e] = s[g][k];
+      for (int k = 0; k < N; ++k) {
+        if constexpr (BVA) {
+          // into this item's consumed A slots of component cc: field g, qy = ky
+          A[(cc * 6 + g) * AV + ((y_qz * Q + k) * NA + y_kx) * EPB + e] = s[g][k];
+        } else {
+          Bv[(cc * 3 + g) * BG + y_qz * BQ + (k * N + y_kx) * EPB + e] = s[g][k];
+        }
+      }
   }
 }
 
 // Z: item (ky, kx) -- z^T sweep of the 3 groups into the element-interleaved
 // E-vector of group grp (the Hessian action's layout)
-template <int N, int Q>
+template <int N, int Q, bool BVA = false>
 __device__ __forceinline__ void xld_z(const double *Bv, double *E, int64_t grp, int item, int e, const Tab &t) {
   using XC = XldCfg<N, Q>;
   constexpr int EPB = XC::EPB, NP = XC::NP, NB = XC::NB;
   constexpr int BQ = NB * EPB, BG = Q * BQ;
+  constexpr int NA = XC::NA, AV = XC::LINES * NA * EPB;
+  const int z_ky = item / N, z_kx = item % N;
   double *out = E + (grp * 3 * NP + item) * EPB + e;
 #pragma unroll
   for (int cc = 0; cc < 3; ++cc) {
@@ -182,10 +206,12 @@ __device__ __forceinline__ void xld_z(const double *Bv, double *E, int64_t grp, 
     for (int k = 0; k < N; ++k) o[k] = 0.0;
 #pragma unroll
     for (int g = 0; g < 3; ++g) {
-      const double *bp = Bv + (cc * 3 + g) * BG + item * EPB + e;
+      // BVA: Bv lives in A (field g, qy = ky) of component cc (xld_y)
+      const double *bp = BVA ? Bv + (cc * 6 + g) * AV + (z_ky * NA + z_kx) * EPB + e
+                             : Bv + (cc * 3 + g) * BG + item * EPB + e;
 #pragma unroll
       for (int qz = 0; qz < Q; ++qz) {
-        const double b = bp[qz * BQ];
+        const double b = bp[qz * (BVA ? Q * NA * EPB : BQ)];
 #pragma unroll
         for (int k = 0; k < N; ++k) o[k] += t.P[g][qz * N + k] * b;
       }
