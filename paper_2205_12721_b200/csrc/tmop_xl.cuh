@@ -81,6 +81,10 @@ struct XlPad {
 #define TMOP_XL_QPF -1
 #endif
 
+// unroll factor of the X stage's point loop (0 = per order)
+#ifndef TMOP_XL_QX_UNROLL
+#define TMOP_XL_QX_UNROLL 0
+#endif
 #ifndef TMOP_XL_GRAD_MINB
 #define TMOP_XL_GRAD_MINB 0
 #endif
@@ -552,10 +556,14 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
           av[c][0][kx] = av[c][1][kx] = av[c][2][kx] = 0.0;
         }
       }
-#pragma unroll
       constexpr bool QPF = APPLY && (TMOP_XL_QPF == 1 || (TMOP_XL_QPF == -1 && N == 4));
       double qnext[11];
       if constexpr (QPF) qload(0, qnext);
+      // (fully unrolled for p <= 2: C3 p = 1 / 2 action 6.57 -> 5.90 / 7.37 -> 7.30 ms,
+      // setup, gradient and energy 2-18 % faster; p = 3 rolled: unrolled, the
+      // action spills, 6.23 -> 7.44 ms)
+      constexpr int QXU = TMOP_XL_QX_UNROLL ? TMOP_XL_QX_UNROLL : (N >= 4 ? 1 : Q);
+#pragma unroll QXU
       for (int qx = 0; qx < Q; ++qx) {
         double tg[N], tb[N];
 #pragma unroll
