@@ -55,8 +55,10 @@ int launch_xl(ElemArgs &a, const Tab &t, cudaStream_t s) {
   using XC = XlCfg<N, Q>;
   constexpr int smem = XC::template smem<KIND>();
   a.ngroups = (a.ne + XC::EPB - 1) / XC::EPB;
-  static_assert(XC::EPB == 16 || XC::EPB == 8 || XC::EPB == 4, "e_es assumes 4-, 8- or 16-element groups");
-  if constexpr (xl_backward<KIND>() || KIND == K_SETUP_DIAG) a.e_es = XC::EPB == 16 ? 4 : XC::EPB == 8 ? 3 : 2;
+  static_assert(XC::EPB == 16 || XC::EPB == 8 || XC::EPB == 4 || XC::EPB == 1,
+                "e_es assumes 1-, 4-, 8- or 16-element groups");
+  if constexpr (xl_backward<KIND>() || KIND == K_SETUP_DIAG)
+    a.e_es = XC::EPB == 16 ? 4 : XC::EPB == 8 ? 3 : XC::EPB == 4 ? 2 : 0;
   auto kfn = xl_kernel<N, Q, KIND>;
   static int per_sm = 0;
   if (per_sm == 0) {
@@ -163,7 +165,8 @@ int launch_one(ElemArgs &a, const Tab &t, cudaStream_t s) {
       }
       return -1;
     } else {
-    if constexpr (DIM == 3 && xl_kind<N, KIND>() && xl_supported<N, Q>()) {
+    if constexpr (DIM == 3 && xl_kind<N, KIND>() && xl_supported<N, Q>() &&
+                  (!xl_ldg<N, Q>() || KIND == K_APPLY)) {
       if (xl_enabled()) return launch_xl<N, Q, KIND>(a, t, s);
     }
     a.ngroups = (a.ne + CF::EPB - 1) / CF::EPB;

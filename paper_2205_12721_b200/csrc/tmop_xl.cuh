@@ -62,14 +62,23 @@ __host__ __device__ constexpr bool xl_qdata() {
 
 // Padded strides (in slots) chosen by tools/xl_banks.py so that every shared
 // access pattern of the kernel is bank-conflict free for the group size.
+// n_q >= 7 (the paper's Kershaw table uses 9): one element per CTA and the
+// Hessian action reads its record straight from global memory (the record,
+// 11 n_q^3 doubles, is too large to stage), Q^2 = 49..81 x-line threads.
+template <int N, int Q>
+__host__ __device__ constexpr bool xl_ldg() { return Q >= 7; }
+
 template <int N, int Q>
 struct XlPad {
-  static constexpr int EPB = xl_epb(N);
-  // EPB = 16: a half-warp is one item x 16 elements -- conflict-free unpadded
-  static constexpr int U_QZ = EPB == 16 ? N * N
+  static constexpr int EPB = xl_ldg<N, Q>() ? 1 : xl_epb(N);
+  // EPB = 16: a half-warp is one item x 16 elements -- conflict-free unpadded;
+  // EPB = 1: a half-warp is 16 consecutive lines (odd W_QY: distinct banks)
+  static constexpr int U_QZ = (EPB == 16 || EPB == 1) ? N * N
                             : EPB == 8 ? (N * N) | (Q & 1) : (N == 4 ? (Q % 4 == 0 ? 16 : 17) : 25);
-  static constexpr int W_QY = EPB == 16 ? N : EPB == 8 ? (N | 1) : ((N == 5 && (Q == 3 || Q == 7)) ? 7 : 5);
+  static constexpr int W_QY = EPB == 16 ? N : (EPB == 8 || EPB == 1) ? (N | 1)
+                                                 : ((N == 5 && (Q == 3 || Q == 7)) ? 7 : 5);
   static constexpr int W_QZ = EPB == 16 ? Q * N
+                            : EPB == 1 ? Q * W_QY
                             : EPB == 8 ? Q * W_QY + ((N & 1) && !(Q & 1) ? 1 : 0)
                                        : (N == 4 ? Q * 5 : (Q == 3 ? 21 : Q == 4 ? 21 : Q == 6 ? 33 : Q * W_QY));
 };
@@ -81,6 +90,18 @@ struct XlPad {
 #define TMOP_XL_QPF -1
 #endif
 
+// x-line Hessian action at n_q >= 7 (xl_ldg): 1 = on, 0 = work-item kernel
+#ifndef TMOP_XL_LDG
+#define TMOP_XL_LDG 1
+#endif
+// (bulk L2 prefetch of the next element's record: measured slower at
+// 24^3 n_q = 9, p = 1 0.242 -> 0.254 ms, with 31 % more DRAM reads)
+#ifndef TMOP_XL_LDG_L2PF
+#define TMOP_XL_LDG_L2PF 0
+#endif
+#ifndef TMOP_XL_LDG_MINB
+#define TMOP_XL_LDG_MINB 0
+#endif
 // unroll factor of the X stage's point loop (0 = per order)
 #ifndef TMOP_XL_QX_UNROLL
 #define TMOP_XL_QX_UNROLL 0
@@ -110,7 +131,8 @@ struct XlCfg {
   static constexpr int W_SZ = 9 * Q * W_QZ;
   static constexpr int SLOTS = (U_SZ + W_SZ + 1) & ~1;
   static constexpr int F = 11;                 // lean fields (T, k0, itau)
-  static constexpr int QS = lean_stride(F * QP, EPB);
+  static constexpr int QS = lean_stride(F * QP, xl_epb(N));   // the record's element stride (Cfg::QS)
+  static constexpr bool LDG = xl_ldg<N, Q>();              // apply: record read from global memory
   static constexpr int XOFF = SLOTS * EPB;                 // gathered input: XS[c][l][e]
   static constexpr int FOFF = XOFF + 3 * NP * EPB;         // fixed-flag words: FS[l][e] (uint32)
   static constexpr int BOFF = FOFF + (NP * EPB + 1) / 2;   // flag byte offsets: FB[l][e] (uint8)
@@ -130,7 +152,7 @@ struct XlCfg {
   static constexpr int SMEM_SD = (QOFF_S + XldCfg<N, Q>::R1OP + XldCfg<N, Q>::BV_SZ * EPB) * 8;
   template <int KIND>
   static constexpr int smem() {
-    return xl_qdata<KIND>() ? SMEM
+    return xl_qdata<KIND>() ? (LDG ? QOFF * 8 : SMEM)
            : (xl_backward<KIND>() ? QOFF * 8
                                   : (KIND == K_SETUP ? SMEM_S : (KIND == K_SETUP_DIAG ? SMEM_SD : SMEM_F)));
   }
@@ -146,6 +168,7 @@ struct XlCfg {
            // p = 1, n_q = 3 action (144-thread CTAs): 3 CTAs / SM at a 128-register cap (small spill)
            // beat 2 CTAs at 166 registers: overlapped apply 6.46 -> 6.12 ms
            : (KIND == K_APPLY && N <= 2 && Q == 3) ? TMOP_XL_P1_MINB
+           : (KIND == K_APPLY && xl_ldg<N, Q>() && TMOP_XL_LDG_MINB) ? TMOP_XL_LDG_MINB
            : (KIND == K_GRAD && TMOP_XL_GRAD_MINB) ? TMOP_XL_GRAD_MINB
                         : cmax(1, 65536 / (WARPS * 32 *
                                            (xl_backward<KIND>() ? (N <= 2 ? 168 : N == 3 ? 248 : 255)
@@ -155,8 +178,15 @@ struct XlCfg {
 
 template <int N, int Q>
 __host__ __device__ constexpr bool xl_supported() {
-  // the CTA's work buffers + staged Q-data within 227 KB
-  return Q >= 2 && XlCfg<N, Q>::SMEM <= 227 * 1024;
+  // the CTA's work buffers + staged Q-data within 227 KB; n_q >= 7: the
+  // Hessian action only (p <= 2), record from global memory
+  if constexpr (xl_ldg<N, Q>()) {
+    // (p = 1 only: 24^3 n_q = 9 action 0.265 -> 0.242 ms; p = 2 slower,
+    // 0.291 -> 0.363 ms at 243 registers, 6 warps / SM)
+    return TMOP_XL_LDG != 0 && N <= 2 && XlCfg<N, Q>::NT <= 1024 && XlCfg<N, Q>::QOFF * 8 <= 227 * 1024;
+  } else {
+    return Q >= 2 && XlCfg<N, Q>::SMEM <= 227 * 1024;
+  }
 }
 
 // Fixed-order block reductions for any CTA size (partial warps allowed):
@@ -379,6 +409,7 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
     xl_kernel(const ElemArgs a, const __grid_constant__ Tab t) {
   using XC = XlCfg<N, Q>;
   constexpr bool APPLY = xl_qdata<KIND>();
+  constexpr bool LDG = APPLY && XC::LDG;   // record fields loaded from global memory (n_q >= 7)
   constexpr bool BACK = xl_backward<KIND>();
   constexpr bool MASK = APPLY;          // the apply zeroes constrained inputs (operator.py:409)
   constexpr bool NTM = KIND == K_APPLY_NT;
@@ -471,13 +502,13 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
     mbar_expect_tx(&qbar, bytes);
     tma_load_1d(QB, a.qdata + e0 * QS, bytes, &qbar);
   };
-  const double *qb = QB + e * QS + lqy + Q * lqz;   // field 0 of point (qx = 0) of this line
+  const double *qb = QB + e * QS + lqy + Q * lqz;   // field 0 of point (qx = 0) of this line (LDG: per group)
   auto qload = [&](int qx, double (&qd)[11]) {
 #pragma unroll
-    for (int f = 0; f < 11; ++f) qd[f] = qb[f * QP + Q * Q * qx];
+    for (int f = 0; f < 11; ++f) qd[f] = LDG ? __ldg(qb + f * QP + Q * Q * qx) : qb[f * QP + Q * Q * qx];
   };
   uint32_t phase = 0;
-  if constexpr (APPLY) {
+  if constexpr (APPLY && !LDG) {
     if (tid == 0) {
       mbar_init(&qbar, 1);
       mbar_fence_init();
@@ -495,6 +526,16 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
     const int64_t eg = grp * EPB + e;
     if constexpr (KIND == K_SETUP) {
       if (tid == 0) bulk_wait_read();   // previous group's record store has read QB
+    }
+    if constexpr (LDG) {
+      // this line's record (global) and the next group's record block -> L2
+      qb = a.qdata + (grp * EPB + e) * QS + lqy + Q * lqz;
+      const int64_t g2 = grp + gridDim.x;
+      if (TMOP_XL_LDG_L2PF && tid == 0 && g2 < a.ngroups) {
+        const int64_t e2 = g2 * EPB;
+        const int64_t cnt = (a.ne - e2) < EPB ? (a.ne - e2) : EPB;
+        l2_prefetch_bulk(a.qdata + e2 * QS, (uint32_t)(cnt * QS * 8));
+      }
     }
     cp_async_wait_all();
     __syncthreads();
@@ -532,7 +573,7 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
     __syncthreads();
     issue_gather();                             // group grp + grid: lands during X / B2 / B1
     load_index(grp + 2 * (int64_t)gridDim.x);   // consumed one group from now
-    if constexpr (APPLY) mbar_wait(&qbar, phase);   // this group's Q-data
+    if constexpr (APPLY && !LDG) mbar_wait(&qbar, phase);   // this group's Q-data
     // ---- X: y-sweep of this line's row qy, x-sweep, point stage,
     // transposed x-sweep -- all in registers
     {
@@ -556,13 +597,13 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
           av[c][0][kx] = av[c][1][kx] = av[c][2][kx] = 0.0;
         }
       }
-      constexpr bool QPF = APPLY && (TMOP_XL_QPF == 1 || (TMOP_XL_QPF == -1 && N == 4));
+      constexpr bool QPF = APPLY && (TMOP_XL_QPF == 1 || (TMOP_XL_QPF == -1 && (N == 4 || LDG)));
       double qnext[11];
       if constexpr (QPF) qload(0, qnext);
       // (fully unrolled for p <= 2: C3 p = 1 / 2 action 6.57 -> 5.90 / 7.37 -> 7.30 ms,
       // setup, gradient and energy 2-18 % faster; p = 3 rolled: unrolled, the
       // action spills, 6.23 -> 7.44 ms)
-      constexpr int QXU = TMOP_XL_QX_UNROLL ? TMOP_XL_QX_UNROLL : (N >= 4 ? 1 : Q);
+      constexpr int QXU = TMOP_XL_QX_UNROLL ? TMOP_XL_QX_UNROLL : ((N >= 4 || XC::LDG) ? 1 : Q);
 #pragma unroll QXU
       for (int qx = 0; qx < Q; ++qx) {
         double tg[N], tb[N];
@@ -611,7 +652,7 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
     }
     if constexpr (BACK) {
       __syncthreads();
-      if constexpr (APPLY) {
+      if constexpr (APPLY && !LDG) {
         // QB is free again: stream in the next group's Q-data
         phase ^= 1u;
         if (tid == 0 && grp + gridDim.x < a.ngroups) issue(grp + gridDim.x);

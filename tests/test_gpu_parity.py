@@ -313,7 +313,7 @@ def test_graph_replayed_minres_matches_eager(rng):
 
 
 @pytest.mark.parametrize("order,nq,counts", [(1, 3, (5, 4, 3)), (2, 4, (6, 3, 4)), (3, 5, (3, 2, 4)),
-                                             (4, 6, (2, 3, 2))])
+                                             (4, 6, (2, 3, 2)), (1, 9, (5, 4, 3))])
 def test_lattice_gather_and_xline_kernels_match_generic(order, nq, counts, rng, monkeypatch):
     """The structured-lattice E->L (tmop_ctx_set_lattice) sums the same copies
     in the same order as the transpose map: bitwise equal results."""
