@@ -102,6 +102,14 @@ struct XlPad {
 #ifndef TMOP_XL_LDG_MINB
 #define TMOP_XL_LDG_MINB 0
 #endif
+// y-sweep results W of the x-line in the thread's own A slots instead of
+// registers (-1 = per configuration, 0 = never, 1 = always)
+#ifndef TMOP_XL_WSM
+#define TMOP_XL_WSM -1
+#endif
+#ifndef TMOP_XL_LDG_NMAX
+#define TMOP_XL_LDG_NMAX 3
+#endif
 // unroll factor of the X stage's point loop (0 = per order)
 #ifndef TMOP_XL_QX_UNROLL
 #define TMOP_XL_QX_UNROLL 0
@@ -168,7 +176,7 @@ struct XlCfg {
            // p = 1, n_q = 3 action (144-thread CTAs): 3 CTAs / SM at a 128-register cap (small spill)
            // beat 2 CTAs at 166 registers: overlapped apply 6.46 -> 6.12 ms
            : (KIND == K_APPLY && N <= 2 && Q == 3) ? TMOP_XL_P1_MINB
-           : (KIND == K_APPLY && xl_ldg<N, Q>() && TMOP_XL_LDG_MINB) ? TMOP_XL_LDG_MINB
+           : (KIND == K_APPLY && xl_ldg<N, Q>()) ? (TMOP_XL_LDG_MINB ? TMOP_XL_LDG_MINB : (N <= 3 ? 4 : 2))
            : (KIND == K_GRAD && TMOP_XL_GRAD_MINB) ? TMOP_XL_GRAD_MINB
                         : cmax(1, 65536 / (WARPS * 32 *
                                            (xl_backward<KIND>() ? (N <= 2 ? 168 : N == 3 ? 248 : 255)
@@ -181,9 +189,10 @@ __host__ __device__ constexpr bool xl_supported() {
   // the CTA's work buffers + staged Q-data within 227 KB; n_q >= 7: the
   // Hessian action only (p <= 2), record from global memory
   if constexpr (xl_ldg<N, Q>()) {
-    // (p = 1 only: 24^3 n_q = 9 action 0.265 -> 0.242 ms; p = 2 slower,
-    // 0.291 -> 0.363 ms at 243 registers, 6 warps / SM)
-    return TMOP_XL_LDG != 0 && N <= 2 && XlCfg<N, Q>::NT <= 1024 && XlCfg<N, Q>::QOFF * 8 <= 227 * 1024;
+    // (24^3 n_q = 9 action p = 1 0.265 -> 0.242 ms; p = 2 0.291 -> 0.284 ms
+    // with W in shared memory at 4 CTAs / SM (0.363 ms with W in registers,
+    // 243 registers, 2 CTAs); p = 3 slower, 0.325 -> 0.50 ms)
+    return TMOP_XL_LDG != 0 && N <= TMOP_XL_LDG_NMAX && XlCfg<N, Q>::NT <= 1024 && XlCfg<N, Q>::QOFF * 8 <= 227 * 1024;
   } else {
     return Q >= 2 && XlCfg<N, Q>::SMEM <= 227 * 1024;
   }
@@ -577,7 +586,9 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
     // ---- X: y-sweep of this line's row qy, x-sweep, point stage,
     // transposed x-sweep -- all in registers
     {
+      constexpr bool WSM = BACK && (TMOP_XL_WSM == 1 || (TMOP_XL_WSM == -1 && LDG && N >= 3));
       double wv[3][3][N], av[3][3][N];
+      double *wo = W + ox;   // (WSM: this thread's own A slots hold W until the x^T output)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const double *ub = U + c * 2 * UV + ou;
@@ -591,9 +602,15 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
             s1 += ty_g[ky] * vb;
             s2 += ty_b[ky] * vg;
           }
-          wv[c][0][kx] = s0;
-          wv[c][1][kx] = s1;
-          wv[c][2][kx] = s2;
+          if constexpr (WSM) {
+            wo[(c * 3 + 0) * WV + kx * EPB] = s0;
+            wo[(c * 3 + 1) * WV + kx * EPB] = s1;
+            wo[(c * 3 + 2) * WV + kx * EPB] = s2;
+          } else {
+            wv[c][0][kx] = s0;
+            wv[c][1][kx] = s1;
+            wv[c][2][kx] = s2;
+          }
           av[c][0][kx] = av[c][1][kx] = av[c][2][kx] = 0.0;
         }
       }
@@ -618,9 +635,15 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
           double s0 = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll
           for (int k = 0; k < N; ++k) {
-            s0 += tg[k] * wv[c][0][k];
-            s1 += tb[k] * wv[c][1][k];
-            s2 += tb[k] * wv[c][2][k];
+            if constexpr (WSM) {
+              s0 += tg[k] * wo[(c * 3 + 0) * WV + k * EPB];
+              s1 += tb[k] * wo[(c * 3 + 1) * WV + k * EPB];
+              s2 += tb[k] * wo[(c * 3 + 2) * WV + k * EPB];
+            } else {
+              s0 += tg[k] * wv[c][0][k];
+              s1 += tb[k] * wv[c][1][k];
+              s2 += tb[k] * wv[c][2][k];
+            }
           }
           g[c][0] = s0;
           g[c][1] = s1;
