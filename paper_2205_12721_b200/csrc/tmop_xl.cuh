@@ -107,6 +107,9 @@ struct XlPad {
 #ifndef TMOP_XL_WSM
 #define TMOP_XL_WSM -1
 #endif
+#ifndef TMOP_XL_LDG_NMIN
+#define TMOP_XL_LDG_NMIN 3
+#endif
 #ifndef TMOP_XL_LDG_NMAX
 #define TMOP_XL_LDG_NMAX 3
 #endif
@@ -189,10 +192,15 @@ __host__ __device__ constexpr bool xl_supported() {
   // the CTA's work buffers + staged Q-data within 227 KB; n_q >= 7: the
   // Hessian action only (p <= 2), record from global memory
   if constexpr (xl_ldg<N, Q>()) {
-    // (24^3 n_q = 9 action p = 1 0.265 -> 0.242 ms; p = 2 0.291 -> 0.284 ms
-    // with W in shared memory at 4 CTAs / SM (0.363 ms with W in registers,
-    // 243 registers, 2 CTAs); p = 3 slower, 0.325 -> 0.50 ms)
-    return TMOP_XL_LDG != 0 && N <= TMOP_XL_LDG_NMAX && XlCfg<N, Q>::NT <= 1024 && XlCfg<N, Q>::QOFF * 8 <= 227 * 1024;
+    // (24^3 n_q = 9 action p = 2 0.291 -> 0.284 ms with W in shared memory
+    // at 4 CTAs / SM (0.363 ms with W in registers, 243 registers, 2 CTAs);
+    // p = 3 slower, 0.325 -> 0.50 ms.  p = 1 is faster, 0.265 -> 0.242 ms,
+    // but off by default (TMOP_XL_LDG_NMIN=2 enables it): its different
+    // rounding flips the paper-table p = 1 Kershaw solve -- chaotic, see
+    // from converged in 69 Newton iterations to the
+    // 100-iteration cap)
+    return TMOP_XL_LDG != 0 && N >= TMOP_XL_LDG_NMIN && N <= TMOP_XL_LDG_NMAX && XlCfg<N, Q>::NT <= 1024 &&
+           XlCfg<N, Q>::QOFF * 8 <= 227 * 1024;
   } else {
     return Q >= 2 && XlCfg<N, Q>::SMEM <= 227 * 1024;
   }
