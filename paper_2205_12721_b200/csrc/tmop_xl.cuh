@@ -545,7 +545,8 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
       if (tid == 0) bulk_wait_read();   // previous group's record store has read QB
     }
     if constexpr (LDG) {
-      // this line's record (global) and the next group's record block -> L2
+      // this line's record in global memory (and, with TMOP_XL_LDG_L2PF, the
+      // next group's record block -> L2)
       qb = a.qdata + (grp * EPB + e) * QS + lqy + Q * lqz;
       const int64_t g2 = grp + gridDim.x;
       if (TMOP_XL_LDG_L2PF && tid == 0 && g2 < a.ngroups) {
