@@ -18,7 +18,7 @@
 namespace tmop {
 
 #ifndef TMOP_XL_GRAD_P3
-#define TMOP_XL_GRAD_P3 0
+#define TMOP_XL_GRAD_P3 1
 #endif
 
 // TMOP_XL=0 forces the work-item kernels (elem_kernel) everywhere (A/B and
@@ -40,8 +40,9 @@ template <int N, int KIND>
 constexpr bool xl_kind() {
   if constexpr (KIND == K_SETUP_DIAG) return N <= 4;
   if constexpr (N >= 5) return KIND == K_ENERGY || KIND == K_MINDET;
-  // p = 3 gradient: the x-line form spills ~320 B per thread at 255
-  // registers; the work-item kernel measured faster (C3: 8.5 vs 9.1 ms)
+  // p = 3 gradient: x-line with W in shared memory (tmop_xl.cuh WSM), C3
+  // 8.3 -> 7.4-7.7 ms; with W in registers it spilled ~320 B per thread at
+  // 255 registers and the work-item kernel was faster (8.5 vs 9.1 ms)
   if constexpr (N == 4 && KIND == K_GRAD) return TMOP_XL_GRAD_P3 != 0;
   return KIND == K_APPLY || KIND == K_APPLY_NT || KIND == K_GRAD || KIND == K_SETUP || KIND == K_ENERGY ||
          KIND == K_MINDET;

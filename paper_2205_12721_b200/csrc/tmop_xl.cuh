@@ -144,6 +144,7 @@ struct XlCfg {
   static constexpr int F = 11;                 // lean fields (T, k0, itau)
   static constexpr int QS = lean_stride(F * QP, xl_epb(N));   // the record's element stride (Cfg::QS)
   static constexpr bool LDG = xl_ldg<N, Q>();              // apply: record read from global memory
+  static constexpr bool GRAD3 = Q == N + 1;                // gradient: W in shared memory, 3 CTAs / SM
   static constexpr int XOFF = SLOTS * EPB;                 // gathered input: XS[c][l][e]
   static constexpr int FOFF = XOFF + 3 * NP * EPB;         // fixed-flag words: FS[l][e] (uint32)
   static constexpr int BOFF = FOFF + (NP * EPB + 1) / 2;   // flag byte offsets: FB[l][e] (uint8)
@@ -181,6 +182,10 @@ struct XlCfg {
            : (KIND == K_APPLY && N <= 2 && Q == 3) ? TMOP_XL_P1_MINB
            : (KIND == K_APPLY && xl_ldg<N, Q>()) ? (TMOP_XL_LDG_MINB ? TMOP_XL_LDG_MINB : (N <= 3 ? 4 : 2))
            : (KIND == K_GRAD && TMOP_XL_GRAD_MINB) ? TMOP_XL_GRAD_MINB
+           // gradient at n_q = p + 2 (W in shared memory): 3 CTAs / SM (p = 3 at
+           // 2 CTAs: 7.5 ms, at 3: 6.7 ms; with W in registers 3 CTAs were slower
+           // at p = 2, 9.6 vs 7.5 ms)
+           : (KIND == K_GRAD && GRAD3) ? 3
                         : cmax(1, 65536 / (WARPS * 32 *
                                            (xl_backward<KIND>() ? (N <= 2 ? 168 : N == 3 ? 248 : 255)
                                                                 : (N <= 3 ? 128 : 168))));
@@ -595,7 +600,11 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
     // ---- X: y-sweep of this line's row qy, x-sweep, point stage,
     // transposed x-sweep -- all in registers
     {
-      constexpr bool WSM = BACK && (TMOP_XL_WSM == 1 || (TMOP_XL_WSM == -1 && LDG && N >= 3));
+      // (per configuration: the n_q >= 7 action, 4 CTAs / SM; the gradient at
+      // n_q = p + 2, 3 CTAs / SM: C3 p = 1 / 2 / 3 5.9 / 8.0 / 8.3 -> 5.4-5.5 /
+      // 7.6-7.7 / 6.7 ms -- p = 3 spilled ~320 B with W in registers)
+      constexpr bool WSM =
+          BACK && (TMOP_XL_WSM == 1 || (TMOP_XL_WSM == -1 && ((LDG && N >= 3) || (KIND == K_GRAD && XC::GRAD3))));
       double wv[3][3][N], av[3][3][N];
       double *wo = W + ox;   // (WSM: this thread's own A slots hold W until the x^T output)
 #pragma unroll
