@@ -113,6 +113,10 @@ struct XlPad {
 #ifndef TMOP_XL_LDG_NMAX
 #define TMOP_XL_LDG_NMAX 3
 #endif
+// (p = 3 action unrolled by 2: C3 6.23 -> 6.14 ms; fully unrolled it spills)
+#ifndef TMOP_XL_P3_APPLY_UNROLL
+#define TMOP_XL_P3_APPLY_UNROLL 2
+#endif
 // unroll factor of the X stage's point loop (0 = per order)
 #ifndef TMOP_XL_QX_UNROLL
 #define TMOP_XL_QX_UNROLL 0
@@ -636,9 +640,10 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
       double qnext[11];
       if constexpr (QPF) qload(0, qnext);
       // (fully unrolled for p <= 2: C3 p = 1 / 2 action 6.57 -> 5.90 / 7.37 -> 7.30 ms,
-      // setup, gradient and energy 2-18 % faster; p = 3 rolled: unrolled, the
-      // action spills, 6.23 -> 7.44 ms)
-      constexpr int QXU = TMOP_XL_QX_UNROLL ? TMOP_XL_QX_UNROLL : ((N >= 4 || XC::LDG) ? 1 : Q);
+      // setup, gradient and energy 2-18 % faster; p = 3: fully unrolled the
+      // action spills, 6.23 -> 7.44 ms, by 2 6.23 -> 6.14 ms)
+      constexpr int QXU = TMOP_XL_QX_UNROLL ? TMOP_XL_QX_UNROLL
+                          : XC::LDG ? 1 : N >= 4 ? (KIND == K_APPLY ? TMOP_XL_P3_APPLY_UNROLL : 1) : Q;
 #pragma unroll QXU
       for (int qx = 0; qx < Q; ++qx) {
         double tg[N], tb[N];
