@@ -113,6 +113,10 @@ struct XlPad {
 #ifndef TMOP_XL_LDG_NMAX
 #define TMOP_XL_LDG_NMAX 3
 #endif
+// (p = 3 gradient unrolled by 2: C3 6.67 -> 6.43 ms; fully: 7.7 ms)
+#ifndef TMOP_XL_P3_GRAD_UNROLL
+#define TMOP_XL_P3_GRAD_UNROLL 2
+#endif
 // (p = 3 action unrolled by 2: C3 6.23 -> 6.14 ms; fully unrolled it spills)
 #ifndef TMOP_XL_P3_APPLY_UNROLL
 #define TMOP_XL_P3_APPLY_UNROLL 2
@@ -643,7 +647,10 @@ __global__ void __launch_bounds__(XlCfg<N, Q>::NT, XlCfg<N, Q>::template minb<KI
       // setup, gradient and energy 2-18 % faster; p = 3: fully unrolled the
       // action spills, 6.23 -> 7.44 ms, by 2 6.23 -> 6.14 ms)
       constexpr int QXU = TMOP_XL_QX_UNROLL ? TMOP_XL_QX_UNROLL
-                          : XC::LDG ? 1 : N >= 4 ? (KIND == K_APPLY ? TMOP_XL_P3_APPLY_UNROLL : 1) : Q;
+                          : XC::LDG ? 1
+                          : N >= 4 ? (KIND == K_APPLY ? TMOP_XL_P3_APPLY_UNROLL
+                                                      : KIND == K_GRAD ? TMOP_XL_P3_GRAD_UNROLL : 1)
+                                   : Q;
 #pragma unroll QXU
       for (int qx = 0; qx < Q; ++qx) {
         double tg[N], tb[N];
